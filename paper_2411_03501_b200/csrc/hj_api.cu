@@ -1,0 +1,91 @@
+// hj_api.cu -- API-surface kernels that are not on the fused stage path:
+// Hamiltonian evaluation on given costates (reachability.py:61-116,
+// term.py:136-140) and divided-difference tables (spatial.py:92-106).
+#include <cstring>
+#include "hj_kernels.cuh"
+
+namespace hj {
+
+struct CostatePtrs {
+  const double* p[HJ_MAX_DIM];
+};
+
+template <int HAM, int DIM>
+__global__ void __launch_bounds__(256) k_eval_ham(const GridArgs G, const hj_ham H, const CostatePtrs C,
+                                                  double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G.cells * G.batch) return;
+  int ix[HJ_MAX_DIM];
+  const long long off = locate(G, idx, ix);
+  double p[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) p[a] = C.p[a][off];
+  out[off] = hamiltonian<HAM, DIM>(H, G.nodes, ix, p);
+}
+
+// One thread per line along `axis`: D0 = single-axis ghost extension
+// (_extend_axis, grid.py:203-225), D1..D3 = successive differences divided by
+// h, 2h, 3h (spatial.py:93-95).  Output oriented with the axis last.
+__global__ void k_divdiff(const GridArgs G, int axis, int w, int order, const double* __restrict__ v,
+                          double* __restrict__ d0, double* __restrict__ d1, double* __restrict__ d2,
+                          double* __restrict__ d3, long long lines) {
+  const long long L = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (L >= lines) return;
+  long long rem = L, base = 0;
+  for (int a = G.dim - 1; a >= 0; --a) {
+    if (a == axis) continue;
+    const long long q = rem / G.n[a];
+    base += (rem - q * G.n[a]) * G.stride[a];
+    rem = q;
+  }
+  const AxisView& A = G.ax[axis];
+  const int n = A.n, ne = n + 2 * w;
+  const double* line = v + base;
+  const Spacing sp = G.sp[axis];
+  double* o0 = d0 + L * ne;
+  double* o1 = d1 + L * (ne - 1);
+  for (int p = 0; p < ne; ++p) o0[p] = fetch(line, A, p - w);
+  for (int p = 0; p < ne - 1; ++p) o1[p] = (o0[p + 1] - o0[p]) / sp.h;
+  if (order >= 2) {
+    double* o2 = d2 + L * (ne - 2);
+    for (int p = 0; p < ne - 2; ++p) o2[p] = (o1[p + 1] - o1[p]) / sp.h2;
+    if (order >= 3) {
+      double* o3 = d3 + L * (ne - 3);
+      for (int p = 0; p < ne - 3; ++p) o3[p] = (o2[p + 1] - o2[p]) / sp.h3;
+    }
+  }
+}
+
+template <int HAM, int DIM>
+static void launch_eval(const GridArgs& G, const hj_ham& H, const CostatePtrs& C, double* out, cudaStream_t s) {
+  const long long total = G.cells * G.batch;
+  k_eval_ham<HAM, DIM><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(G, H, C, out);
+}
+
+cudaError_t launch_eval_ham(const GridArgs& G, const hj_ham& H, const double* const* p, double* out,
+                            cudaStream_t s) {
+  CostatePtrs C{};
+  for (int a = 0; a < G.dim; ++a) C.p[a] = p[a];
+  switch (H.kind) {
+    case HJ_HAM_ADVECTION:
+      if (G.dim == 1) launch_eval<HJ_HAM_ADVECTION, 1>(G, H, C, out, s);
+      else if (G.dim == 2) launch_eval<HJ_HAM_ADVECTION, 2>(G, H, C, out, s);
+      else if (G.dim == 3) launch_eval<HJ_HAM_ADVECTION, 3>(G, H, C, out, s);
+      else launch_eval<HJ_HAM_ADVECTION, 4>(G, H, C, out, s);
+      break;
+    case HJ_HAM_ROCKETS: launch_eval<HJ_HAM_ROCKETS, 3>(G, H, C, out, s); break;
+    case HJ_HAM_ROCKETS_EXTREMAL: launch_eval<HJ_HAM_ROCKETS_EXTREMAL, 3>(G, H, C, out, s); break;
+    case HJ_HAM_AIR3D: launch_eval<HJ_HAM_AIR3D, 3>(G, H, C, out, s); break;
+    default: launch_eval<HJ_HAM_DI4, 4>(G, H, C, out, s); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_divdiff(const GridArgs& G, int axis, int w, int order, const double* v, double* d0,
+                           double* d1, double* d2, double* d3, cudaStream_t s) {
+  const long long lines = G.cells / G.n[axis];
+  k_divdiff<<<(unsigned)((lines + 127) / 128), 128, 0, s>>>(G, axis, w, order, v, d0, d1, d2, d3, lines);
+  return cudaGetLastError();
+}
+
+}  // namespace hj

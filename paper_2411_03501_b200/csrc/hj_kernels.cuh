@@ -1,0 +1,96 @@
+// hj_kernels.cuh -- kernel argument blocks shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include "hj_ham.cuh"
+
+namespace hj {
+
+// Device view of hj_grid: owned extents, element strides, per-axis ghost rules.
+struct GridArgs {
+  int dim;
+  int batch;
+  int n[HJ_MAX_DIM];
+  long long stride[HJ_MAX_DIM];
+  long long batch_stride;
+  long long cells;        // owned nodes of one problem
+  AxisView ax[HJ_MAX_DIM];
+  Spacing sp[HJ_MAX_DIM];
+  const double* nodes[HJ_MAX_DIM];
+};
+
+struct StageArgs {
+  GridArgs g;
+  hj_ham ham;
+  double alpha_half[HJ_MAX_DIM];  // alphas[i] * 0.5 (term.py:86)
+  double dt;
+  int stage;
+  int mask;
+  int eps_mode;
+  int want_ranges;
+  int tag;
+  const double* y_in;
+  const double* y0;
+  double* y_out;
+  const double* mask_prev;
+  hj_stats* stats;
+};
+
+// Split a linear owned-node index into (problem, per-axis indices) and the
+// element offset of that node from the problem-0 base pointer.
+__device__ __forceinline__ long long locate(const GridArgs& g, long long idx, int* ix) {
+  long long rem = idx;
+  long long off = 0;
+  for (int a = g.dim - 1; a >= 0; --a) {
+    const long long q = rem / g.n[a];
+    ix[a] = (int)(rem - q * g.n[a]);
+    off += (long long)ix[a] * g.stride[a];
+    rem = q;
+  }
+  return off + rem * g.batch_stride;
+}
+
+// Block-wide reduction of the non-finite flags and optional costate ranges
+// into the device hj_stats (one atomic per block and quantity).
+template <int DIM>
+__device__ __forceinline__ void reduce_stats(hj_stats* st, unsigned flags, int tag, bool want_ranges,
+                                             long long* lo, long long* hi) {
+  const unsigned any = __any_sync(0xffffffffu, flags != 0u);
+  if (any) {
+    unsigned f = flags;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+    if ((threadIdx.x & 31) == 0) {
+      atomicOr(&st->nonfinite, f);
+      atomicMin(&st->first_bad_tag, tag);
+    }
+  }
+  if (!want_ranges) return;
+  __shared__ long long s_lo[HJ_MAX_DIM][32];
+  __shared__ long long s_hi[HJ_MAX_DIM][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    long long l = lo[a], h = hi[a];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
+      h = max(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    if (lane == 0) { s_lo[a][warp] = l; s_hi[a][warp] = h; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      long long l = s_lo[a][0], h = s_hi[a][0];
+      for (int w = 1; w < nw; ++w) { l = min(l, s_lo[a][w]); h = max(h, s_hi[a][w]); }
+      atomicMin((long long*)&st->lo_key[a], l);
+      atomicMax((long long*)&st->hi_key[a], h);
+    }
+  }
+}
+
+constexpr long long KEY_POS_INF = 0x7ff0000000000000LL;                 // order_key(+inf)
+constexpr long long KEY_NEG_INF = (long long)0xfff0000000000000ULL ^ 0x7fffffffffffffffLL;  // order_key(-inf)
+
+}  // namespace hj

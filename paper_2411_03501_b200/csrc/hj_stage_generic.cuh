@@ -1,0 +1,89 @@
+// hj_stage_generic.cuh -- the generic fused grid-update kernel (one launch
+// per TVD-RK stage), instantiated per Hamiltonian in hj_stage_*.cu.
+//
+// Fused pass per node (term.py:90-126 + integrator.py:92-103):
+//   ghosts (grid.py:203-225) -> per-axis upwind pair (spatial.py:119-247)
+//   -> p_avg = 0.5*(L+R) (term.py:101) -> H(x, p_avg) (device functor)
+//   -> diss = sum (alpha_i*0.5)*(R_i-L_i) (term.py:84-86) -> delta = diss - H
+//   -> stage update -> optional tube mask (reachability.py:249) -> store.
+#pragma once
+#include "hj_kernels.cuh"
+
+namespace hj {
+
+template <int DIM, int SCHEME, int HAM>
+__global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
+  constexpr int W = Width<SCHEME>::value;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = P.g.cells * P.g.batch;
+  unsigned flags = 0u;
+  long long lo[DIM], hi[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) { lo[a] = KEY_POS_INF; hi[a] = KEY_NEG_INF; }
+
+  if (idx < total) {
+    int ix[HJ_MAX_DIM];
+    const long long off = locate(P.g, idx, ix);
+    double pbar[DIM];
+    double diss = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const AxisView& A = P.g.ax[a];
+      const double* line = P.y_in + (off - (long long)ix[a] * A.stride);
+      double u[7];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        if (k >= 3 - W && k <= 3 + W) u[k] = fetch(line, A, ix[a] - 3 + k);
+        else u[k] = 0.0;
+      }
+      const LR lr = scheme_lr<SCHEME>(u, P.g.sp[a], P.eps_mode);
+      if (!finite(lr.l) || !finite(lr.r)) flags |= HJ_NF_DERIV;
+      if (P.want_ranges) {
+        lo[a] = min(order_key(lr.l), order_key(lr.r));
+        hi[a] = max(order_key(lr.l), order_key(lr.r));
+      }
+      pbar[a] = 0.5 * (lr.l + lr.r);
+      diss = diss + P.alpha_half[a] * (lr.r - lr.l);
+    }
+    const double H = hamiltonian<HAM, DIM>(P.ham, P.g.nodes, ix, pbar);
+    if (!finite(H)) flags |= HJ_NF_HAM;
+    if (H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
+    const double delta = diss - H;
+    if (!finite(delta)) flags |= HJ_NF_DELTA;
+    const double y = P.y_in[off];
+    if (!finite(y)) flags |= HJ_NF_INPUT;
+    const double y0 = (P.stage >= HJ_STAGE_RK2_AVG) ? P.y0[off] : 0.0;
+    double out = stage_update(P.stage, P.dt, y, y0, delta);
+    if (P.mask == HJ_MASK_MIN) {
+      const double pv = P.mask_prev[off];
+      out = (pv < out) ? pv : out;
+    } else if (P.mask == HJ_MASK_MAX) {
+      const double pv = P.mask_prev[off];
+      out = (pv > out) ? pv : out;
+    }
+    if (!finite(out)) flags |= HJ_NF_OUTPUT;
+    P.y_out[off] = out;
+  }
+  if (P.stats) reduce_stats<DIM>(P.stats, flags, P.tag, P.want_ranges != 0, lo, hi);
+}
+
+// ------------------------------------------------------------------ launchers
+template <int DIM, int SCHEME, int HAM>
+static inline cudaError_t launch_stage_t(const StageArgs& P, cudaStream_t s) {
+  const long long total = P.g.cells * P.g.batch;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  k_stage_generic<DIM, SCHEME, HAM><<<blocks, 256, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int DIM, int HAM>
+static inline cudaError_t launch_stage_s(int scheme, const StageArgs& P, cudaStream_t s) {
+  switch (scheme) {
+    case HJ_FIRST: return launch_stage_t<DIM, HJ_FIRST, HAM>(P, s);
+    case HJ_ENO2: return launch_stage_t<DIM, HJ_ENO2, HAM>(P, s);
+    case HJ_ENO3: return launch_stage_t<DIM, HJ_ENO3, HAM>(P, s);
+    default: return launch_stage_t<DIM, HJ_WENO5, HAM>(P, s);
+  }
+}
+
+}  // namespace hj
