@@ -130,7 +130,9 @@ typedef struct hj_stats {
   int64_t lo_key[HJ_MAX_DIM];
   int64_t hi_key[HJ_MAX_DIM];
   uint32_t nonfinite;                 /* OR of HJ_NF_* bits                                 */
-  int32_t first_bad_tag;              /* min tag of a stage that saw a non-finite value     */
+  int32_t first_bad_tag;              /* min over failing nodes of tag*8 + error class
+                                         (1 input, 2 derivative, 3 H, 4 delta, 5 output);
+                                         0x7fffffff when nothing failed                    */
 } hj_stats;
 
 /* ---------------------------------------------------------------- meta */

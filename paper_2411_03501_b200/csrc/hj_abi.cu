@@ -59,7 +59,7 @@ static int cuda_status(cudaError_t e, const char* what, uint64_t launches = 1) {
 }
 
 // hj_grid -> GridArgs, with the reference's validation (grid.py:117-175, spatial.py:74-81).
-static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G) {
+static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G, unsigned ghost_axes = 0xffu) {
   if (!g) return fail(HJ_EINVAL, "grid is NULL");
   if (g->dim < 1 || g->dim > 4) return fail(HJ_EINVAL, "grid dim %d unsupported (1..4)", g->dim);
   if (g->batch < 1) return fail(HJ_EINVAL, "batch must be >= 1, got %d", g->batch);
@@ -89,11 +89,11 @@ static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G) {
     A.halo_hi = (a == 0) ? g->halo_hi : 0;
     if (A.bc < HJ_BC_PERIODIC || A.bc > HJ_BC_DIRICHLET)
       return fail(HJ_EINVAL, "axis %d: unknown boundary kind %d", a, A.bc);
-    if ((A.halo_lo || A.halo_hi) && g->halo < ghost_width)
+    if (((ghost_axes >> a) & 1u) && (A.halo_lo || A.halo_hi) && g->halo < ghost_width)
       return fail(HJ_EINVAL, "axis 0 halo %d thinner than ghost width %d", g->halo, ghost_width);
-    if (ghost_width > 0 && A.bc == HJ_BC_PERIODIC && !(A.halo_lo && A.halo_hi) && ghost_width > A.n)
+    if (((ghost_axes >> a) & 1u) && ghost_width > 0 && A.bc == HJ_BC_PERIODIC && !(A.halo_lo && A.halo_hi) && ghost_width > A.n)
       return fail(HJ_EINVAL, "ghost width %d exceeds %d nodes on periodic axis %d", ghost_width, A.n, a);
-    if (ghost_width > 0 && A.bc == HJ_BC_EXTRAPOLATE && A.n < 2 && !(A.halo_lo && A.halo_hi))
+    if (((ghost_axes >> a) & 1u) && ghost_width > 0 && A.bc == HJ_BC_EXTRAPOLATE && A.n < 2 && !(A.halo_lo && A.halo_hi))
       return fail(HJ_EINVAL, "axis %d: extrapolation needs at least 2 nodes", a);
     if (!(g->h[a] > 0.0)) return fail(HJ_EINVAL, "axis %d: spacing must be positive", a);
     G->sp[a].h = g->h[a];
@@ -102,6 +102,12 @@ static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G) {
     G->nodes[a] = g->nodes[a];
   }
   return HJ_OK;
+}
+
+static bool all_zero(const double* alpha, int dim) {
+  for (int a = 0; a < dim; ++a)
+    if (alpha[a] != 0.0) return false;
+  return true;
 }
 
 static int ghost_width_of(int scheme) {
@@ -164,7 +170,7 @@ int hj_derivs(const hj_grid* g, int scheme, int axis, int eps_mode, const double
   const int w = ghost_width_of(scheme);
   if (w < 0) return fail(HJ_EINVAL, "unknown derivative scheme %d", scheme);
   GridArgs G;
-  int rc = make_grid(g, w, &G);
+  int rc = make_grid(g, w, &G, 1u << (axis & 7));
   if (rc) return rc;
   if (axis < 0 || axis >= G.dim) return fail(HJ_EINVAL, "axis %d out of range for dim %d", axis, G.dim);
   if (eps_mode != HJ_EPS_SQUARED && eps_mode != HJ_EPS_RAW) return fail(HJ_EINVAL, "eps_mode must be 'squared' or 'raw'");
@@ -175,7 +181,7 @@ int hj_derivs(const hj_grid* g, int scheme, int axis, int eps_mode, const double
 int hj_weno5_workspace(const hj_grid* g, int axis, int side, int eps_mode, const double* v, double* ws,
                        void* stream) {
   GridArgs G;
-  int rc = make_grid(g, 3, &G);
+  int rc = make_grid(g, 3, &G, 1u << (axis & 7));
   if (rc) return rc;
   if (axis < 0 || axis >= G.dim) return fail(HJ_EINVAL, "axis %d out of range for dim %d", axis, G.dim);
   if (side != 0 && side != 1) return fail(HJ_EINVAL, "side must be 'left' or 'right'");
@@ -213,6 +219,7 @@ int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alph
   P.mask = mask;
   P.eps_mode = HJ_EPS_SQUARED;  // derivative_pair passes no eps_mode (spatial.py:276)
   P.want_ranges = 0;
+  P.want_hnz = stats && all_zero(alpha, P.g.dim);
   P.tag = tag;
   P.y_in = y_in;
   P.y0 = y0;
@@ -248,6 +255,7 @@ int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha
   P.stage = HJ_STAGE_DELTA;
   P.eps_mode = HJ_EPS_SQUARED;
   P.want_ranges = stats ? 1 : 0;
+  P.want_hnz = stats && all_zero(alpha, P.g.dim);
   P.tag = 0;
   P.y_in = v;
   P.y_out = delta;
@@ -357,7 +365,7 @@ int hj_divided_differences(const hj_grid* g, int axis, int width, int order, con
   if (order < 1 || order > 3) return fail(HJ_EINVAL, "order must be 1..3, got %d", order);
   if (width < 1) return fail(HJ_EINVAL, "ghost width must be >= 1, got %d", width);
   GridArgs G;
-  int rc = make_grid(g, width, &G);
+  int rc = make_grid(g, width, &G, 1u << (axis & 7));
   if (rc) return rc;
   if (axis < 0 || axis >= G.dim) return fail(HJ_EINVAL, "axis %d out of range for dim %d", axis, G.dim);
   if (G.batch != 1 || g->halo_lo || g->halo_hi) return fail(HJ_EINVAL, "divided_differences takes one un-haloed field");

@@ -27,6 +27,7 @@ struct StageArgs {
   int mask;
   int eps_mode;
   int want_ranges;
+  int want_hnz;       // record HJ_FLAG_HAM_NONZERO (only needed when every alpha is 0)
   int tag;
   const double* y_in;
   const double* y0;
@@ -51,17 +52,34 @@ __device__ __forceinline__ long long locate(const GridArgs& g, long long idx, in
 
 // Block-wide reduction of the non-finite flags and optional costate ranges
 // into the device hj_stats (one atomic per block and quantity).
+// Error class of a node's flags in the order the reference would raise them
+// (input field, derivative fields, H, delta, output field); 7 = no error.
+__device__ __forceinline__ int error_code(unsigned flags) {
+  if (flags & HJ_NF_INPUT) return 1;
+  if (flags & HJ_NF_DERIV) return 2;
+  if (flags & HJ_NF_HAM) return 3;
+  if (flags & HJ_NF_DELTA) return 4;
+  if (flags & HJ_NF_OUTPUT) return 5;
+  return 7;
+}
+
+// first_bad_tag keeps min(tag*8 + error_code) over every failing node, so the
+// host recovers the first failing stage AND the error it would have raised.
 template <int DIM>
 __device__ __forceinline__ void reduce_stats(hj_stats* st, unsigned flags, int tag, bool want_ranges,
                                              long long* lo, long long* hi) {
   const unsigned any = __any_sync(0xffffffffu, flags != 0u);
   if (any) {
     unsigned f = flags;
+    int key = (flags & 31u) ? tag * 8 + error_code(flags) : 0x7fffffff;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      f |= __shfl_xor_sync(0xffffffffu, f, o);
+      key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+    }
     if ((threadIdx.x & 31) == 0) {
       atomicOr(&st->nonfinite, f);
-      atomicMin(&st->first_bad_tag, tag);
+      if (key != 0x7fffffff) atomicMin(&st->first_bad_tag, key);
     }
   }
   if (!want_ranges) return;

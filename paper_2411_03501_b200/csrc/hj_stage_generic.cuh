@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
     }
     const double H = hamiltonian<HAM, DIM>(P.ham, P.g.nodes, ix, pbar);
     if (!finite(H)) flags |= HJ_NF_HAM;
-    if (H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
+    if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
     const double delta = diss - H;
     if (!finite(delta)) flags |= HJ_NF_DELTA;
     const double y = P.y_in[off];

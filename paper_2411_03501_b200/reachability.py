@@ -1,0 +1,250 @@
+"""Two-rocket game and the backward reachable tube -- drop-in for hjls.reachability.
+
+``solve_brt`` keeps the reference's semantics (reachability.py:218-254): per
+interval, integrate the Lax-Friedrichs term with TVD-RK3, then mask against
+the previous snapshot (min for "over", max for "under").  With a registered
+device Hamiltonian the tube lives in HBM for the whole solve; every RK stage
+is one fused kernel and the mask is fused into the interval's last stage.
+Snapshots are copied to the host once per interval (they are the result).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from . import device as dev
+from .grid import Grid, ScalarField
+from .integrator import IntegrationResult, IntegratorOptions, LaxFriedrichsRHS, ode_cfl_3
+from .term import DeviceHamiltonian, RangeFreePartials, TermConfig
+
+
+@dataclass(frozen=True)
+class RocketParams:
+    """Shared rocket constants, feet/second (reachability.py:33-47)."""
+
+    a: float = 1.0
+    grav: float = 32.0
+    capture_radius: float = 1.5
+    u_min: float = -1.0
+    u_max: float = 1.0
+
+    def __post_init__(self) -> None:
+        if self.a <= 0 or self.grav <= 0 or self.capture_radius <= 0:
+            raise ValueError("a, grav and capture_radius must be positive")
+        if not self.u_min < self.u_max:
+            raise ValueError(f"need u_min < u_max, got [{self.u_min}, {self.u_max}]")
+
+
+def _theta_tables(g: Grid):
+    # reachability.py:60-61: cos/sin of the heading nodes taken on the host with
+    # the reference's own NumPy expression, so the device sees the same bits
+    theta = g.axis_nodes[2].reshape(1, 1, -1)
+    return np.cos(theta).ravel(), np.sin(theta).ravel()
+
+
+class RocketsHamiltonian(DeviceHamiltonian):
+    """Device functor for the published closed form (reachability.py:61-81) or
+    the extremal-control form (reachability.py:84-116)."""
+
+    dim = 3
+
+    def __init__(self, params: RocketParams, route: str = "published"):
+        if route not in ("published", "extremal"):
+            raise ValueError(f"hamiltonian must be 'published' or 'extremal', got {route!r}")
+        self.rp = params
+        self.route = route
+        self.kind = _lib.HAM_ROCKETS if route == "published" else _lib.HAM_ROCKETS_EXTREMAL
+
+    def params(self):
+        return (self.rp.a, self.rp.grav, self.rp.u_min, self.rp.u_max)
+
+    def tables(self, g):
+        return _theta_tables(g)
+
+    def check_grid(self, g):
+        if g.dim != 3:
+            raise ValueError(f"expected 3 costate fields, got {g.dim}")
+
+
+class RocketsPartials(RangeFreePartials):
+    """rockets_partials as a range-free bound (reachability.py:139-157)."""
+
+    def __init__(self, params: RocketParams):
+        self.rp = params
+
+    def alphas(self, t, g):
+        return np.array([rockets_partials(t, g, None, None, a, self.rp) for a in range(3)])
+
+
+def rockets_hamiltonian(t: float, g: Grid, v, p: Sequence[ScalarField], params: RocketParams) -> ScalarField:
+    """H = -a p1 cos(th) - p2 (grav - a - a sin(th)) - u_max|p1 x + p3| + u_min|p2 x + p3|."""
+    if len(p) != 3:
+        raise ValueError(f"expected 3 costate fields, got {len(p)}")
+    return RocketsHamiltonian(params, "published")(t, g, v, p)
+
+
+def rockets_hamiltonian_extremal(t: float, g: Grid, v, p: Sequence[ScalarField],
+                                 params: RocketParams) -> ScalarField:
+    """Extremal-control Hamiltonian (reachability.py:84-116)."""
+    if len(p) != 3:
+        raise ValueError(f"expected 3 costate fields, got {len(p)}")
+    return RocketsHamiltonian(params, "extremal")(t, g, v, p)
+
+
+def rockets_hamiltonian_oracle(t: float, state: Sequence[float], p: Sequence[float],
+                               params: RocketParams) -> float:
+    """-max_{u_e} min_{u_p} p . f over the four control corners (reachability.py:119-136).
+
+    A scalar test oracle of the reference, kept as plain host arithmetic (it
+    is not part of the grid-update path)."""
+    x, _, theta = (float(s) for s in state)
+    p1, p2, p3 = (float(c) for c in p)
+    a, g = params.a, params.grav
+    best_e = -np.inf
+    for u_e in (params.u_min, params.u_max):
+        best_p = np.inf
+        for u_p in (params.u_min, params.u_max):
+            fx = a * np.cos(theta) + u_e * x
+            fz = a * np.sin(theta) + a + u_p * x - g
+            ft = u_p - u_e
+            best_p = min(best_p, p1 * fx + p2 * fz + p3 * ft)
+        best_e = max(best_e, best_p)
+    return -best_e
+
+
+def rockets_partials(t: float, g: Grid, v, ranges, axis: int, params: RocketParams) -> float:
+    """Global |dH/dp_axis| bounds, independent of the ranges (reachability.py:139-157)."""
+    a, grav = params.a, params.grav
+    x_max = float(max(abs(g.mins[0]), abs(g.maxs[0])))
+    if axis == 0:
+        return a + abs(params.u_max) * x_max
+    if axis == 1:
+        return max(abs(grav), abs(grav - 2.0 * a)) + abs(params.u_min) * x_max
+    if axis == 2:
+        return abs(params.u_max) + abs(params.u_min)
+    raise ValueError(f"axis {axis} out of range for the 3-state rockets game")
+
+
+def rockets_term_config(params: RocketParams, scheme: str = "eno2", hamiltonian: str = "published") -> TermConfig:
+    """Bundle a rockets Hamiltonian route with its bounds (reachability.py:160-183)."""
+    if hamiltonian not in ("published", "extremal"):
+        raise ValueError(f"hamiltonian must be 'published' or 'extremal', got {hamiltonian!r}")
+    return TermConfig(hamiltonian=RocketsHamiltonian(params, hamiltonian), partials=RocketsPartials(params),
+                      derivative_scheme=scheme)
+
+
+@dataclass(frozen=True)
+class ReachProblem:
+    """Grid, target level function, term wiring, horizon (reachability.py:186-207)."""
+
+    grid: Grid
+    target: ScalarField
+    params: RocketParams
+    term_config: TermConfig
+    horizon: float
+    global_steps: int
+
+    def __post_init__(self) -> None:
+        if self.grid.dim != 3:
+            raise ValueError(f"rockets game needs a 3-D grid, got dim {self.grid.dim}")
+        if not self.grid.is_periodic(2):
+            raise ValueError("the heading axis (axis 2) must be periodic")
+        if not self.target.matches(self.grid):
+            raise ValueError("target field does not match the grid")
+        if self.horizon < 0:
+            raise ValueError(f"horizon must be nonnegative, got {self.horizon}")
+        if self.global_steps < 1:
+            raise ValueError(f"need at least one global step, got {self.global_steps}")
+
+
+@dataclass(frozen=True)
+class BRTResult:
+    """Tube snapshots, the first at lookback time 0 (reachability.py:210-215)."""
+
+    snapshots: tuple[ScalarField, ...]
+    times: tuple[float, ...]
+
+
+def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
+               opts: IntegratorOptions | None = None,
+               progress: Callable[[int, float, ScalarField], None] | None = None) -> BRTResult:
+    """The tube driver of solve_brt for any dimension and RK order.
+
+    ReachProblem insists on the 3-D rockets layout and solve_brt hard-wires
+    RK3 (reachability.py:198-199, 246); this is the same loop with those two
+    choices opened up (Air3D C1 runs RK2, the 4-D pair runs on 4 axes).
+    """
+    if horizon == 0:
+        return BRTResult(snapshots=(target,), times=(0.0,))
+    opts = opts or IntegratorOptions()
+    use_min = cfg.approximation_sign == "over"
+    snaps = [target]
+    times = [0.0]
+    if cfg.on_device:
+        from .engine import FusedIntegrator
+
+        fi = FusedIntegrator(g, cfg)
+        prev = dev.to_dev(target.values)
+        for k in range(1, global_steps + 1):
+            t0 = times[-1]
+            t1 = horizon * k / global_steps
+            try:
+                res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
+            except Exception as err:
+                raise RuntimeError(f"tube interval {k} failed: {err}") from err
+            prev = res.y
+            v = ScalarField(dev.to_host(prev))
+            snaps.append(v)
+            times.append(t1)
+            if progress is not None:
+                progress(k, t1, v)
+        return BRTResult(snapshots=tuple(snaps), times=tuple(times))
+
+    from .integrator import ode_cfl_1, ode_cfl_2
+
+    integ = {1: ode_cfl_1, 2: ode_cfl_2, 3: ode_cfl_3}[order]
+    rhs = LaxFriedrichsRHS(g)
+    v = target
+    for k in range(1, global_steps + 1):
+        t0 = times[-1]
+        t1 = horizon * k / global_steps
+        try:
+            res: IntegrationResult = integ(rhs, (t0, t1), v, opts, cfg)
+        except Exception as err:
+            raise RuntimeError(f"tube interval {k} failed: {err}") from err
+        y = dev.to_dev(res.y_final.values)
+        dev.mask_dev(y, dev.to_dev(snaps[-1].values), use_min)
+        v = ScalarField(dev.to_host(y))
+        snaps.append(v)
+        times.append(t1)
+        if progress is not None:
+            progress(k, t1, v)
+    return BRTResult(snapshots=tuple(snaps), times=tuple(times))
+
+
+def solve_brt(problem: ReachProblem, opts: IntegratorOptions | None = None,
+              progress: Callable[[int, float, ScalarField], None] | None = None) -> BRTResult:
+    """Grow the backward reachable tube over ``global_steps`` equal intervals
+    with TVD-RK3 and per-interval masking (reachability.py:218-254)."""
+    return solve_tube(problem.grid, problem.target, problem.term_config, problem.horizon, problem.global_steps,
+                      order=3, opts=opts, progress=progress)
+
+
+def sublevel_volume(g: Grid, f: ScalarField, level: float = 0.0) -> float:
+    """Volume of {f < level}, one cell per node (reachability.py:257-260); the
+    count runs on the GPU."""
+    cell = float(np.prod(g.spacings))
+    return cell * float(dev.count_below_dev(dev.to_dev(f.values), level))
+
+
+__all__ = [
+    "BRTResult", "ReachProblem", "RocketParams", "RocketsHamiltonian", "RocketsPartials", "rockets_hamiltonian",
+    "rockets_hamiltonian_extremal", "rockets_hamiltonian_oracle", "rockets_partials", "rockets_term_config",
+    "solve_brt", "solve_tube", "sublevel_volume",
+]
+
+_ = math
