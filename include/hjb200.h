@@ -216,6 +216,9 @@ int hj_mask(int64_t count, const double* prev, double* v, int mask, void* stream
 /* reachability.py:257-260: *d_count += #{v < level} */
 int hj_count_below(int64_t count, const double* v, double level,
                    unsigned long long* d_count, void* stream);
+/* Self-check of the hoisted-reciprocal division used by the fast kernels:
+ * n random/special operand pairs, *d_mismatch += #{div_by(a,b) != a/b} (bitwise). */
+int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);
 /* zero a device hj_stats (keys set to +inf/-inf images) */
 int hj_stats_reset(hj_stats* stats, void* stream);
 

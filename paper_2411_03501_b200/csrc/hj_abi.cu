@@ -31,6 +31,7 @@ cudaError_t launch_rk_combine(long long n, int stage, double dt, const double* y
                               const double* delta, double* out, hj_stats* st, int tag, cudaStream_t s);
 cudaError_t launch_eval_ham(const GridArgs& G, const hj_ham& H, const double* const* p, double* out,
                             cudaStream_t s);
+cudaError_t launch_check_division(long long n, unsigned long long seed, unsigned long long* mism, cudaStream_t s);
 cudaError_t launch_divdiff(const GridArgs& G, int axis, int w, int order, const double* v, double* d0,
                            double* d1, double* d2, double* d3, cudaStream_t s);
 }  // namespace hj
@@ -340,6 +341,11 @@ int hj_count_below(int64_t count, const double* v, double level, unsigned long l
   if (!v || !d_count) return fail(HJ_EINVAL, "NULL pointer");
   if (count <= 0) return HJ_OK;
   return cuda_status(launch_count_below(count, v, level, d_count, (cudaStream_t)stream), "hj_count_below");
+}
+
+int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream) {
+  if (!d_mismatch || n < 0) return fail(HJ_EINVAL, "bad arguments");
+  return cuda_status(launch_check_division(n, seed, d_mismatch, (cudaStream_t)stream), "hj_check_division");
 }
 
 int hj_stats_reset(hj_stats* stats, void* stream) {

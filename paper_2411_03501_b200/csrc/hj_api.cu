@@ -56,6 +56,54 @@ __global__ void k_divdiff(const GridArgs G, int axis, int w, int order, const do
   }
 }
 
+// ---- self-check of div_by (hoisted reciprocal) against IEEE '/', bit for bit
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__device__ double random_operand(unsigned long long r, unsigned long long s) {
+  const unsigned sel = (unsigned)(s % 64);
+  switch (sel) {
+    case 0: return 0.0;
+    case 1: return -0.0;
+    case 2: return __longlong_as_double((long long)(r & 0x000fffffffffffffull));            // subnormal
+    case 3: return __longlong_as_double((long long)((r & 0x800fffffffffffffull) | (1ull << 52)));  // tiny normal
+    case 4: return __longlong_as_double((long long)((r & 0x800fffffffffffffull) | (0x7feull << 52))); // huge
+    case 5: return 3.0;
+    case 6: return 6.0;
+    case 7: return 0.1;
+    case 8: return INFINITY;
+    default: break;
+  }
+  // random sign/mantissa, exponent mostly in the range the solver sees, sometimes anywhere
+  unsigned long long e = (sel < 48) ? (1023ull - 80ull + (s >> 8) % 160ull) : ((s >> 8) % 2047ull);
+  return __longlong_as_double((long long)((r & 0x800fffffffffffffull) | (e << 52)));
+}
+
+__global__ void k_check_division(long long n, unsigned long long seed, unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = seed ^ (unsigned long long)i * 0x2545f4914f6cdd1dull;
+    const double a = random_operand(splitmix(k), splitmix(k + 1));
+    const double b = random_operand(splitmix(k + 2), splitmix(k + 3));
+    const double q1 = div_by(a, make_recip(b));
+    const double q2 = a / b;
+    const bool same = (__double_as_longlong(q1) == __double_as_longlong(q2)) || (isnan(q1) && isnan(q2));
+    bad += same ? 0ull : 1ull;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+cudaError_t launch_check_division(long long n, unsigned long long seed, unsigned long long* mism, cudaStream_t s) {
+  k_check_division<<<148 * 8, 256, 0, s>>>(n, seed, mism);
+  return cudaGetLastError();
+}
+
 template <int HAM, int DIM>
 static void launch_eval(const GridArgs& G, const hj_ham& H, const CostatePtrs& C, double* out, cudaStream_t s) {
   const long long total = G.cells * G.batch;

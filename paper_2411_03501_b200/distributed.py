@@ -1,0 +1,225 @@
+"""Slab domain decomposition of the grid-update path across GPUs.
+
+Axis 0 is split into contiguous slabs, one per rank (one process per GPU,
+torch.distributed / NCCL over NVLink for the plumbing).  Each rank's state
+buffer holds ``halo`` exchanged planes in front of and behind its owned
+planes; the fused stage kernels read those planes where a single-GPU run
+would read its neighbours' nodes, and synthesise the boundary ghosts only on
+the global edges.  Per stage: one grouped send/recv of ``halo`` planes with
+each neighbour, then the stage kernel.  Because the halos are exact copies
+and every node update is local to its star stencil, the decomposed result is
+bit-identical to the single-GPU one.  Dissipation bounds are global and
+range-free, so dt needs no collective; non-finite flags are max-reduced once
+per interval.
+
+Transports: ``TorchDistTransport`` (NCCL or gloo process group) for real
+ranks; ``LocalTransport`` runs all slabs of one process on one device with
+plain copies (tests / emulation -- no kernel ever waits on another).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+from .engine import FusedIntegrator
+from .term import TermConfig
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    world: int
+    lo: int          # first owned global plane
+    n: int           # owned planes
+    halo: int
+    has_lo: bool     # a neighbour provides planes below lo
+    has_hi: bool     # a neighbour provides planes above lo + n
+    lo_rank: int
+    hi_rank: int
+
+
+def partition(n0: int, world: int, halo: int, periodic: bool) -> list[Slab]:
+    """Balanced contiguous split of axis 0; every slab must hold >= halo planes
+    (its boundary planes are a neighbour's halo) and >= 2 (extrapolation)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    base, extra = divmod(n0, world)
+    sizes = [base + (1 if r < extra else 0) for r in range(world)]
+    if world > 1 and min(sizes) < max(halo, 2):
+        raise ValueError(f"axis 0 has {n0} nodes: too few for {world} slabs with halo {halo}")
+    slabs, lo = [], 0
+    for r, n in enumerate(sizes):
+        has_lo = world > 1 and (r > 0 or periodic)
+        has_hi = world > 1 and (r < world - 1 or periodic)
+        slabs.append(Slab(r, world, lo, n, halo, has_lo, has_hi, (r - 1) % world, (r + 1) % world))
+        lo += n
+    return slabs
+
+
+def halo_plan(s: Slab):
+    """Halo messages of one slab in buffer-plane coordinates (buffer plane p =
+    owned plane p - halo).  Returns (sends, recvs): sends ordered [to lower,
+    to upper], recvs ordered [from upper, from lower].  With that order the
+    k-th send from A to B always pairs with B's k-th receive from A, even when
+    the lower and upper neighbour are the same rank (two periodic slabs)."""
+    h = s.halo
+    sends, recvs = [], []
+    if s.has_lo:   # my first h owned planes become the lower neighbour's upper halo
+        sends.append((s.lo_rank, (h, 2 * h)))
+    if s.has_hi:   # my last h owned planes become the upper neighbour's lower halo
+        sends.append((s.hi_rank, (s.n, s.n + h)))
+    if s.has_hi:
+        recvs.append((s.hi_rank, (s.n + h, s.n + 2 * h)))
+    if s.has_lo:
+        recvs.append((s.lo_rank, (0, h)))
+    return sends, recvs
+
+
+class TorchDistTransport:
+    """Halo exchange through a torch.distributed process group (NCCL on GPUs)."""
+
+    def __init__(self, slab: Slab, group=None):
+        self.slab = slab
+        self.group = group
+
+    def exchange(self, buf: torch.Tensor) -> None:
+        import torch.distributed as dist
+
+        sends, recvs = halo_plan(self.slab)
+        ops = [dist.P2POp(dist.isend, buf[a:b], peer, self.group) for peer, (a, b) in sends]
+        ops += [dist.P2POp(dist.irecv, buf[a:b], peer, self.group) for peer, (a, b) in recvs]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def max_flags(self, flags: int) -> int:
+        import torch.distributed as dist
+
+        t = torch.tensor([int(flags)], dtype=torch.int64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+
+class SlabIntegrator(FusedIntegrator):
+    """FusedIntegrator on one slab of a decomposed grid.
+
+    State tensors are FULL buffers of shape (halo + n + halo, n1, ...); the
+    owned region is ``buf[halo:halo+n]``.  ``step3`` / ``integrate`` take and
+    return full buffers.
+    """
+
+    def __init__(self, g, cfg: TermConfig, rank: int, world: int, halo: int = 3, transport=None, group=None):
+        self.slab = partition(g.counts[0], world, halo, g.is_periodic(0))[rank]
+        s = self.slab
+        dg = dev.DeviceGrid(g, slab=(s.lo, s.n, int(s.has_lo), int(s.has_hi), s.halo))
+        self.transport = transport or TorchDistTransport(s, group)
+        super().__init__(g, cfg, dg=dg, exchange=None)
+        self.full_shape = (s.n + 2 * s.halo,) + tuple(g.counts[1:])
+        self.owned_cells = dg.cells
+
+    # -- buffers ---------------------------------------------------------
+    def empty(self) -> torch.Tensor:
+        return torch.zeros(self.full_shape, dtype=dev.F64, device=dev.device())
+
+    def owned(self, buf: torch.Tensor) -> torch.Tensor:
+        h = self.slab.halo
+        return buf[h:h + self.slab.n]
+
+    def init_shape(self, kind: int, params) -> torch.Tensor:
+        buf = self.empty()
+        self.owned(buf).copy_(dev.init_shape_dev(self.dg, kind, params))
+        return buf
+
+    def init_cylinder(self, radius: float, center=(0.0, 0.0, 0.0), ignore_mask: int = 4) -> torch.Tensor:
+        return self.init_shape(_lib.SHAPE_CYLINDER, [*center, float(radius), float(ignore_mask)])
+
+    def scatter(self, full: np.ndarray) -> torch.Tensor:
+        buf = self.empty()
+        self.owned(buf).copy_(dev.to_dev(full[self.slab.lo:self.slab.lo + self.slab.n]))
+        return buf
+
+    # -- stage plumbing ----------------------------------------------------
+    def _buffers(self, like: torch.Tensor) -> list[torch.Tensor]:
+        if not self._bufs:
+            self._bufs = [self.empty() for _ in range(3)]
+        return self._bufs
+
+    def _stage(self, alphas_c, dt, kind, y_in, y0, y_out, mask_prev, mask, tag, strm):
+        self.transport.exchange(y_in)
+        o = self.owned
+        dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, o(y_in), None if y0 is None else o(y0),
+                      o(y_out), None if mask_prev is None else o(mask_prev), mask, self.stats, tag, lib=self.lib,
+                      strm=strm)
+        self.launches += 1
+
+    def _raise_pending(self, times, warn: bool = False) -> None:
+        # every rank raises the same error: flags are max-reduced first
+        st = self.stats.read()
+        merged = self.transport.max_flags(st.nonfinite)
+        if merged & _lib.NF_MASK and not st.nonfinite & _lib.NF_MASK:
+            raise RuntimeError("non-finite values on another slab")
+        super()._raise_pending(times, warn)
+
+
+class LocalTransport:
+    """All slabs of a decomposition in one process on one device: before each
+    stage every slab registers its input buffer, then each slab pulls its
+    halos from the neighbours' buffers with plain device copies.  Emulation
+    for tests -- kernels never wait on one another."""
+
+    def __init__(self, slabs: list[Slab]):
+        self.slabs = slabs
+        self.buffers: dict[int, torch.Tensor] = {}
+        self.flags: dict[int, int] = {}
+
+    def register(self, rank: int, buf: torch.Tensor) -> None:
+        self.buffers[rank] = buf
+
+    def for_rank(self, rank: int) -> "_LocalEndpoint":
+        return _LocalEndpoint(self, rank)
+
+
+class _LocalEndpoint:
+    def __init__(self, hub: LocalTransport, rank: int):
+        self.hub, self.rank = hub, rank
+
+    def exchange(self, buf: torch.Tensor) -> None:
+        s = self.hub.slabs[self.rank]
+        h = s.halo
+        _, recvs = halo_plan(s)
+        for peer, (a, b) in recvs:
+            src = self.hub.buffers[peer]
+            p = self.hub.slabs[peer]
+            if a == 0:   # lower halo <- lower neighbour's last h owned planes
+                buf[a:b].copy_(src[p.n:p.n + h])
+            else:        # upper halo <- upper neighbour's first h owned planes
+                buf[a:b].copy_(src[h:2 * h])
+
+    def max_flags(self, flags: int) -> int:
+        self.hub.flags[self.rank] = flags
+        return max(self.hub.flags.values())
+
+
+def lockstep_step3(runs: list[SlabIntegrator], hub: LocalTransport, ys: list[torch.Tensor], t: float,
+                   dt: float) -> list[torch.Tensor]:
+    """One TVD-RK3 step of every slab, stage by stage (LocalTransport runs)."""
+    from .engine import _STAGES
+
+    bufs = [r._buffers(y) for r, y in zip(runs, ys)]
+    outs = [[b for b in bs if b is not y][:2] for bs, y in zip(bufs, ys)]
+    alphas = [_lib.doubles(r._alphas(t, y), _lib.HJ_MAX_DIM) for r, y in zip(runs, ys)]
+    src = list(ys)
+    for k, kind in enumerate(_STAGES[3]):
+        dst = [(o[0], o[1], o[0])[k] for o in outs]
+        for r in range(len(runs)):
+            hub.register(r, src[r])
+        for r, run in enumerate(runs):
+            run._stage(alphas[r], dt, kind, src[r], ys[r] if k else None, dst[r], None, _lib.MASK_NONE, k,
+                       dev.stream())
+        src = dst
+    return src

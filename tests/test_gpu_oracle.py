@@ -42,7 +42,7 @@ def _grid(spec):
 @pytest.mark.parametrize("scheme", ["first", "eno2", "eno3", "weno5"])
 def test_derivatives_random(spec, scheme):
     g = _grid(spec)
-    rng = np.random.default_rng(hash((scheme, tuple(spec["counts"]))) % 2 ** 32)
+    rng = np.random.default_rng([len(scheme), *spec["counts"]])
     v = rng.standard_normal(g.counts) * rng.uniform(0.1, 10.0)
     v[tuple(slice(0, 3) for _ in range(g.dim))] = 0.0   # exact zeros / ties in the ENO picks
     for axis in range(g.dim):
