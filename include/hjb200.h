@@ -219,6 +219,9 @@ int hj_count_below(int64_t count, const double* v, double level,
 /* Self-check of the hoisted-reciprocal division used by the fast kernels:
  * n random/special operand pairs, *d_mismatch += #{div_by(a,b) != a/b} (bitwise). */
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);
+/* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
+ * iters x 8 independent DFMA chains (time it with events on `stream`). */
+int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream);
 /* zero a device hj_stats (keys set to +inf/-inf images) */
 int hj_stats_reset(hj_stats* stats, void* stream);
 

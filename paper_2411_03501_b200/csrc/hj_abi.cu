@@ -32,6 +32,7 @@ cudaError_t launch_rk_combine(long long n, int stage, double dt, const double* y
 cudaError_t launch_eval_ham(const GridArgs& G, const hj_ham& H, const double* const* p, double* out,
                             cudaStream_t s);
 cudaError_t launch_check_division(long long n, unsigned long long seed, unsigned long long* mism, cudaStream_t s);
+cudaError_t launch_fp64_probe(int iters, int blocks, double* out, cudaStream_t s);
 cudaError_t launch_divdiff(const GridArgs& G, int axis, int w, int order, const double* v, double* d0,
                            double* d1, double* d2, double* d3, cudaStream_t s);
 }  // namespace hj
@@ -346,6 +347,11 @@ int hj_count_below(int64_t count, const double* v, double level, unsigned long l
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream) {
   if (!d_mismatch || n < 0) return fail(HJ_EINVAL, "bad arguments");
   return cuda_status(launch_check_division(n, seed, d_mismatch, (cudaStream_t)stream), "hj_check_division");
+}
+
+int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream) {
+  if (iters < 1 || blocks < 1 || !d_sink) return fail(HJ_EINVAL, "bad arguments");
+  return cuda_status(launch_fp64_probe(iters, blocks, d_sink, (cudaStream_t)stream), "hj_fp64_probe");
 }
 
 int hj_stats_reset(hj_stats* stats, void* stream) {

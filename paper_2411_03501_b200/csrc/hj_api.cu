@@ -104,6 +104,27 @@ cudaError_t launch_check_division(long long n, unsigned long long seed, unsigned
   return cudaGetLastError();
 }
 
+// ---- FP64 pipe probe: 8 independent DFMA chains per thread, full chip
+__global__ void __launch_bounds__(256) k_fp64_probe(int iters, double seed, double* out) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed + k + threadIdx.x * 1e-3;
+  const double b = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;   // keep the chains alive
+}
+
+cudaError_t launch_fp64_probe(int iters, int blocks, double* out, cudaStream_t s) {
+  k_fp64_probe<<<blocks, 256, 0, s>>>(iters, 1.0, out);
+  return cudaGetLastError();
+}
+
 template <int HAM, int DIM>
 static void launch_eval(const GridArgs& G, const hj_ham& H, const CostatePtrs& C, double* out, cudaStream_t s) {
   const long long total = G.cells * G.batch;

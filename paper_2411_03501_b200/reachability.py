@@ -226,6 +226,43 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
     return BRTResult(snapshots=tuple(snaps), times=tuple(times))
 
 
+def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
+                     opts: IntegratorOptions | None = None, keep_snapshots: bool = True):
+    """A batch of independent tubes sharing grid and dynamics (BASELINE C5:
+    the flock of Air3D problems).  Dissipation bounds and dt depend on the
+    grid and Hamiltonian only, so the batch advances in lockstep: every stage
+    of every problem is one kernel launch over the stacked (B, n0, ...)
+    state.  Returns (snapshots (global_steps+1, B, *counts) | final (B, ...),
+    times)."""
+    if not cfg.on_device:
+        raise TypeError("solve_tube_batch needs a registered device Hamiltonian")
+    from .engine import FusedIntegrator
+
+    tgt = np.stack([np.asarray(t.values if isinstance(t, ScalarField) else t, dtype=np.float64) for t in targets])
+    if tgt.shape[1:] != tuple(g.counts):
+        raise ValueError(f"targets have shape {tgt.shape[1:]}, grid needs {g.counts}")
+    if not np.isfinite(tgt).all():
+        raise ValueError("field contains non-finite values")
+    opts = opts or IntegratorOptions()
+    dg = dev.DeviceGrid(g, batch=tgt.shape[0])
+    fi = FusedIntegrator(g, cfg, dg=dg)
+    prev = dev.to_dev(tgt)
+    snaps = [tgt] if keep_snapshots else []
+    times = [0.0]
+    use_min = cfg.approximation_sign == "over"
+    for k in range(1, global_steps + 1):
+        t0, t1 = times[-1], horizon * k / global_steps
+        try:
+            res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
+        except Exception as err:
+            raise RuntimeError(f"tube interval {k} failed: {err}") from err
+        prev = res.y
+        if keep_snapshots:
+            snaps.append(dev.to_host(prev))
+        times.append(t1)
+    return (np.stack(snaps) if keep_snapshots else dev.to_host(prev)), tuple(times)
+
+
 def solve_brt(problem: ReachProblem, opts: IntegratorOptions | None = None,
               progress: Callable[[int, float, ScalarField], None] | None = None) -> BRTResult:
     """Grow the backward reachable tube over ``global_steps`` equal intervals
