@@ -3,6 +3,7 @@
 // term.py:136-140) and divided-difference tables (spatial.py:92-106).
 #include <cstring>
 #include "hj_kernels.cuh"
+#include "hj_weno_line.cuh"
 
 namespace hj {
 
@@ -85,6 +86,13 @@ __device__ double random_operand(unsigned long long r, unsigned long long s) {
 
 __global__ void k_check_division(long long n, unsigned long long seed, unsigned long long* mismatches) {
   unsigned long long bad = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the compile-time reciprocals of the WENO kernels must equal make_recip
+    const Recip a = make_recip(3.0), b = make_recip(6.0), c = recip_three(), d = recip_six();
+    bad += (__double_as_longlong(a.r) != __double_as_longlong(c.r)) ? 1000000ull : 0ull;
+    bad += (__double_as_longlong(b.r) != __double_as_longlong(d.r)) ? 1000000ull : 0ull;
+    bad += (a.bhi != c.bhi || b.bhi != d.bhi) ? 1000000ull : 0ull;
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long k = seed ^ (unsigned long long)i * 0x2545f4914f6cdd1dull;
     const double a = random_operand(splitmix(k), splitmix(k + 1));

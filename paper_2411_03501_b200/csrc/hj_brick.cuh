@@ -1,23 +1,23 @@
 // hj_brick.cuh -- the fused LF + TVD-RK stage on 3-D grids, brick-tiled,
 // templated on the upwind scheme and the device Hamiltonian.
 //
-// One CTA (256 threads, ~100 KB shared memory, 2 CTAs per SM) owns an
+// One CTA (256 threads, ~110 KB shared memory, 2 CTAs per SM) owns an
 // 8 x 16 x 16 brick (axes 0, 1, 2).  Per stage and brick:
-//   axis 0: thread (y,x) walks its 8-node column straight from global memory
-//           (coalesced over x; exchanged halo planes / boundary ghosts via
-//           fetch) and parks the values in shared memory;
-//   axis 1: thread (z, segment, x) walks 8 nodes along y in shared memory;
-//   axis 2: thread (z, segment, y) walks 8 nodes along x in shared memory;
-//   every walk stores p_avg_a = 0.5*(L+R) and accumulates the dissipation
-//   d = (0 + d0) + d1 + d2 with d_a = (alpha_a*0.5)*(R_a-L_a) in the
-//   reference's axis order (term.py:84-86);
-//   out:    coalesced pass per node -- H(x, p_avg), delta = d - H
-//           (term.py:113), stage update (integrator.py:93-103), optional
-//           tube mask (reachability.py:249), non-finite flags, store.
-// The three axis walks run through ONE inlined copy of the line walker (a
-// runtime-configured loop over the axes), keeping the kernel's instruction
-// footprint small; the walker itself is a rolled loop with a register window
-// (hj_weno_line.cuh / hj_eno_line.cuh) that computes each face quantity once.
+//   load:   the brick's values, their axis-1/axis-2 halos and the 3+3 axis-0
+//           halo planes go to shared memory (coalesced; exchanged halo planes
+//           or boundary ghosts through fetch());
+//   axis 0: thread (y,x) walks its 8-node column, axis 1: thread (z,seg,x)
+//           walks 8 nodes along y, axis 2: thread (z,seg,y) walks 8 nodes
+//           along x -- every walk from shared memory through ONE inlined copy
+//           of the line walker (a runtime-configured loop over the axes);
+//           each stores p_avg_a = 0.5*(L+R) and accumulates the dissipation
+//           d = ((0 + d0) + d1) + d2, d_a = (alpha_a*0.5)*(R_a-L_a), in the
+//           reference's axis order (term.py:84-86);
+//   out:    per node, coalesced -- H(x, p_avg), delta = d - H (term.py:113),
+//           stage update (integrator.py:93-103), optional tube mask
+//           (reachability.py:249), non-finite flags, store.
+// The line walker (hj_weno_line.cuh / hj_eno_line.cuh) is a rolled loop with a
+// register window that computes every face quantity of its line once.
 #pragma once
 #include "hj_eno_line.cuh"
 #include "hj_kernels.cuh"
@@ -31,16 +31,22 @@ constexpr int SEG = 8;                 // nodes per thread walk along axes 1 and
 constexpr int HB = 3;                  // ghost width held in shared memory (WENO5/ENO3 need 3)
 constexpr int SVP = BYX + 2 * HB + 1;  // 23: odd pitch (conflict-free LDS.64 across y-lanes)
 constexpr int SVR = BYX + 2 * HB;      // 22 rows per plane
-constexpr int SAP = BYX + 1;           // 17: odd pitch of the per-node arrays
+constexpr int PLANE = SVR * SVP;       // doubles per plane of v
+constexpr int NODES = BZ * BYX * BYX;  // 2048 nodes per brick
 constexpr int BRICK_THREADS = 256;
 
 struct BrickSmem {
-  double v[BZ][SVR][SVP];    // brick values with axis-1/axis-2 halos
-  double p0[BZ][BYX][SAP];   // p_avg per axis
-  double p1[BZ][BYX][SAP];
-  double p2[BZ][BYX][SAP];
-  double d[BZ][BYX][SAP];    // running dissipation
+  double v[BZ * PLANE];      // brick planes with axis-1 / axis-2 halos
+  double zh[2 * HB * BYX * BYX];  // axis-0 halo planes: 3 below, 3 above (interior y,x)
+  double p0[NODES];          // p_avg per axis (swizzled node index)
+  double p1[NODES];
+  double p2[NODES];
+  double d[NODES];           // running dissipation
 };
+
+// node (z, y, x) of the brick -> slot in the per-node arrays; the XOR keeps
+// LDS/STS conflict-free whether the lanes of a warp vary x or y
+__device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
 template <int SCHEME, class Load, class Emit>
 __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
@@ -66,117 +72,99 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   const int z0 = bz * BZ, y0 = blockIdx.y * BYX, x0 = blockIdx.x * BYX;
   const long long base = (long long)b * G.batch_stride;
   const double* __restrict__ vin = P.y_in + base;
+  const long long s0 = G.stride[0], s1 = G.stride[1];
   const int t = threadIdx.x;
   unsigned flags = 0u;
 
-  // ---- axis-1 / axis-2 halos of the brick's planes (ghost rules via fetch)
-  for (int q = t; q < BZ * 12 * BYX; q += BRICK_THREADS) {
-    const int z = q / (12 * BYX), r = q % (12 * BYX);
-    const int gz = z0 + z;
-    if (r < 6 * BYX) {           // rows y in {-3..-1, 16..18}, x interior
-      const int k = r / BYX, x = r % BYX;
-      const int y = (k < 3) ? (k - 3) : (BYX + k - 3);
-      const int gx = x0 + x;
-      double val = 0.0;
-      if (gz < n0 && gx < n2) val = fetch(vin + (long long)gz * G.stride[0] + gx, G.ax[1], y0 + y);
-      S.v[z][y + HB][x + HB] = val;
-    } else {                     // columns x in {-3..-1, 16..18}, y interior
-      const int rr = r - 6 * BYX;
-      const int k = rr / BYX, y = rr % BYX;
-      const int x = (k < 3) ? (k - 3) : (BYX + k - 3);
-      const int gy = y0 + y;
-      double val = 0.0;
-      if (gz < n0 && gy < n1)
-        val = fetch(vin + (long long)gz * G.stride[0] + (long long)gy * G.stride[1], G.ax[2], x0 + x);
-      S.v[z][y + HB][x + HB] = val;
+  // ---- load: brick planes with axis-1/axis-2 halos (corners unused)
+  for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
+    const int z = q / (SVR * SVR), r = q % (SVR * SVR);
+    const int yy = r / SVR, xx = r % SVR;
+    const bool yin = yy >= HB && yy < HB + BYX, xin = xx >= HB && xx < HB + BYX;
+    if (!yin && !xin) continue;
+    const int gz = z0 + z, gy = y0 + yy - HB, gx = x0 + xx - HB;
+    double val = 0.0;
+    const bool gy_in = gy >= 0 && gy < n1, gx_in = gx >= 0 && gx < n2;
+    if (gz < n0) {
+      if (gy_in && gx_in) val = vin[gz * s0 + gy * s1 + gx];
+      else if (gx_in) val = fetch(vin + gz * s0 + gx, G.ax[1], gy);        // axis-1 ghost
+      else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, G.ax[2], gx);   // axis-2 ghost
+    } else if (gy_in && gx_in) {
+      val = fetch(vin + gy * s1 + gx, G.ax[0], gz);                         // axis-0 ghost (partial brick)
     }
+    S.v[z * PLANE + yy * SVP + xx] = val;
   }
-  {
-    // in-brick columns past the domain edge of a partial brick: valid nodes
-    // read them as ghosts of axis 1 (gy >= n1) or axis 2 (gx >= n2)
-    const int y = t / BYX, x = t % BYX;
+  // ---- load: axis-0 halo planes (exchanged planes or boundary ghosts)
+  for (int q = t; q < 2 * HB * BYX * BYX; q += BRICK_THREADS) {
+    const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
+    const int y = yx / BYX, x = yx % BYX;
     const int gy = y0 + y, gx = x0 + x;
-    if (gy >= n1 || gx >= n2) {
-      for (int k = 0; k < BZ; ++k) {
-        const int gz = z0 + k;
-        double val = 0.0;
-        if (gz < n0 && gx < n2) val = fetch(vin + (long long)gz * G.stride[0] + gx, G.ax[1], gy);
-        else if (gz < n0 && gy < n1)
-          val = fetch(vin + (long long)gz * G.stride[0] + (long long)gy * G.stride[1], G.ax[2], gx);
-        S.v[k][y + HB][x + HB] = val;
-      }
-    }
+    const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+    double val = 0.0;
+    if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, G.ax[0], e);
+    S.zh[q] = val;
   }
+  __syncthreads();
 
-  // ---- the three axis walks through one copy of the line walker
-#pragma unroll 1
-  for (int ax = 0; ax < 3; ++ax) {
-    const double* src;          // line start (relative node 0)
-    long long sstride;          // element stride along the line
-    bool from_global;
-    int e0 = 0;                 // global index of relative node 0 (axis-0 walk)
-    double* op;                 // p_avg output, node 0
-    double* od;                 // dissipation, node 0
-    int ostride;
-    int nvalid;                 // nodes [0, nvalid) are inside the domain
-    int len;
-    double* park = nullptr;
-    if (ax == 0) {
-      const int y = t / BYX, x = t % BYX;
-      const int gy = y0 + y, gx = x0 + x;
-      src = vin + (long long)gy * G.stride[1] + gx;
-      sstride = 0;
-      from_global = true;
-      e0 = z0;
-      park = &S.v[0][y + HB][x + HB];
-      op = &S.p0[0][y][x];
-      od = &S.d[0][y][x];
-      ostride = BYX * SAP;
-      len = BZ;
-      nvalid = (gy < n1 && gx < n2) ? min(BZ, n0 - z0) : -1;
-    } else if (ax == 1) {
-      const int x = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-      src = &S.v[z][HB + seg * SEG][x + HB];
-      sstride = SVP;
-      from_global = false;
-      op = &S.p1[z][seg * SEG][x];
-      od = &S.d[z][seg * SEG][x];
-      ostride = SAP;
-      len = SEG;
-      nvalid = (z0 + z < n0 && x0 + x < n2) ? min(SEG, n1 - (y0 + seg * SEG)) : 0;
-    } else {
-      const int y = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-      src = &S.v[z][y + HB][HB + seg * SEG];
-      sstride = 1;
-      from_global = false;
-      op = &S.p2[z][y][seg * SEG];
-      od = &S.d[z][y][seg * SEG];
-      ostride = 1;
-      len = SEG;
-      nvalid = (z0 + z < n0 && y0 + y < n1) ? min(SEG, n2 - (x0 + seg * SEG)) : 0;
-    }
-    if (nvalid >= 0) {   // axis-0 walks skip columns outside the domain
-      const AxisView A0 = G.ax[0];
-      const double ah = P.alpha_half[ax];
-      const bool first = ax == 0;
+  // ---- axis 0: thread (y, x) walks its column (zh planes below / above)
+  {
+    const int y = t / BYX, x = t % BYX;
+    if (y0 + y < n1 && x0 + x < n2) {
+      const int nvalid = min(BZ, n0 - z0);
+      const double* col = &S.v[(y + HB) * SVP + (x + HB)];
+      const double* zlo = &S.zh[HB * BYX * BYX + y * BYX + x];          // plane k+3, k in [-3,-1]
+      const double* zhi = &S.zh[(HB - BZ) * BYX * BYX + y * BYX + x];   // plane k-BZ+3, k >= BZ
+      const double ah = P.alpha_half[0];
+      const int s00 = swz(0, y, x);
       auto ld = [&](int k) -> double {
-        if (from_global) {
-          const double val = fetch(src, A0, e0 + k);
-          if (k >= 0 && k < BZ) park[k * (SVR * SVP)] = val;
-          return val;
-        }
-        return src[k * sstride];
+        if (k < 0) return zlo[k * (BYX * BYX)];
+        if (k < BZ) return col[k * PLANE];
+        return zhi[k * (BYX * BYX)];
       };
       auto emit = [&](int i, double L, double R) {
         if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
-        op[i * ostride] = 0.5 * (L + R);                     // term.py:101
-        const double prev = first ? 0.0 : od[i * ostride];   // term.py:84 zeros
-        od[i * ostride] = prev + ah * (R - L);               // term.py:85-86
+        const int s = s00 + i * (BYX * BYX);
+        S.p0[s] = 0.5 * (L + R);                               // term.py:101
+        S.d[s] = 0.0 + ah * (R - L);                           // term.py:84-86 (from zeros)
       };
-      line_walk<SCHEME>(ld, len, G.sp[ax], emit);
+      line_walk<SCHEME>(ld, BZ, G.sp[0], emit);
     }
-    __syncthreads();
   }
+  __syncthreads();
+  // ---- axis 1: thread (z, seg, x) walks SEG nodes along y
+  {
+    const int x = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
+    const int nvalid = (z0 + z < n0 && x0 + x < n2) ? min(SEG, n1 - (y0 + seg * SEG)) : 0;
+    const double* line = &S.v[z * PLANE + (HB + seg * SEG) * SVP + (x + HB)];
+    const double ah = P.alpha_half[1];
+    const int ybase = seg * SEG;
+    auto ld = [&](int k) -> double { return line[k * SVP]; };
+    auto emit = [&](int i, double L, double R) {
+      if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
+      const int s = swz(z, ybase + i, x);
+      S.p1[s] = 0.5 * (L + R);
+      S.d[s] = S.d[s] + ah * (R - L);
+    };
+    line_walk<SCHEME>(ld, SEG, G.sp[1], emit);
+  }
+  __syncthreads();
+  // ---- axis 2: thread (z, seg, y) walks SEG nodes along x
+  {
+    const int y = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
+    const int nvalid = (z0 + z < n0 && y0 + y < n1) ? min(SEG, n2 - (x0 + seg * SEG)) : 0;
+    const double* line = &S.v[z * PLANE + (y + HB) * SVP + (HB + seg * SEG)];
+    const double ah = P.alpha_half[2];
+    const int row = (z * BYX + y) * BYX, xbase = seg * SEG;
+    auto ld = [&](int k) -> double { return line[k]; };
+    auto emit = [&](int i, double L, double R) {
+      if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
+      const int s = row + ((xbase + i) ^ y);
+      S.p2[s] = 0.5 * (L + R);
+      S.d[s] = S.d[s] + ah * (R - L);
+    };
+    line_walk<SCHEME>(ld, SEG, G.sp[2], emit);
+  }
+  __syncthreads();
 
   // ---- per node: H, delta, stage update, mask, store (coalesced over axis 2)
   {
@@ -184,22 +172,23 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
     const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
     double* __restrict__ out = P.y_out + base;
 #pragma unroll 2
-    for (int q = t; q < BZ * BYX * BYX; q += BRICK_THREADS) {
+    for (int q = t; q < NODES; q += BRICK_THREADS) {
       const int z = q / (BYX * BYX), y = (q / BYX) % BYX, x = q % BYX;
       const int gz = z0 + z, gy = y0 + y, gx = x0 + x;
       if (gz >= n0 || gy >= n1 || gx >= n2) continue;
-      const long long off = (long long)gz * G.stride[0] + (long long)gy * G.stride[1] + gx;
+      const long long off = gz * s0 + gy * s1 + gx;
+      const int s = swz(z, y, x);
       double p[3];
-      p[0] = S.p0[z][y][x];
-      p[1] = S.p1[z][y][x];
-      p[2] = S.p2[z][y][x];
+      p[0] = S.p0[s];
+      p[1] = S.p1[s];
+      p[2] = S.p2[s];
       const int ix[3] = {gz, gy, gx};
       const double H = hamiltonian<HAM, 3>(P.ham, G.nodes, ix, p);
       if (!finite(H)) flags |= HJ_NF_HAM;
       if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
-      const double delta = S.d[z][y][x] - H;                // term.py:113
+      const double delta = S.d[s] - H;                          // term.py:113
       if (!finite(delta)) flags |= HJ_NF_DELTA;
-      const double yv = S.v[z][y + HB][x + HB];
+      const double yv = S.v[z * PLANE + (y + HB) * SVP + (x + HB)];
       if (!finite(yv)) flags |= HJ_NF_INPUT;
       const double yz = (P.stage >= HJ_STAGE_RK2_AVG) ? y0p[off] : 0.0;
       double o = stage_update(P.stage, P.dt, yv, yz, delta);
@@ -227,8 +216,8 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = true;
   }

@@ -1,9 +1,10 @@
-# A/B of the stage kernels + correctness, one GPU call
+# A/B of the stage kernels + correctness + profile, one GPU call
 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/smoke.log 2>&1
-for v in generic brick brick1; do
+for v in generic brick; do
   HJ_STAGE_KERNEL=$v timeout 300 python bench.py --steps 6 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_$v.log 2>&1
 done
-timeout 1200 python -m pytest tests/test_gpu_golden.py tests/test_gpu_oracle.py tests/test_gpu_distributed.py tests/test_gpu_batch.py tests/test_gpu_division.py -q -p no:cacheprovider --timeout 600 -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_brick -s 2 -c 1 -o gpurun_out/prof_brick3 python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_brick -s 2 -c 1 -o gpurun_out/prof_brick5 python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+timeout 600 python scripts/bench_configs.py c1 c5 c2s > gpurun_out/configs.log 2>&1
 echo done
