@@ -105,6 +105,31 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def fp64_peak(dev, lib):
+    """Measured FP64-pipe throughput (DFMA lane-ops/s) from hj_fp64_probe:
+    148*8 CTAs x 256 threads x 8 independent DFMA chains."""
+    import torch
+
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, iters = 148 * 8, 4096
+    lib.hj_fp64_probe(iters, blocks, sink.data_ptr(), dev.stream())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    lib.hj_fp64_probe(iters, blocks, sink.data_ptr(), dev.stream())
+    e.record()
+    torch.cuda.synchronize()
+    return blocks * 256 * iters * 8 / (s.elapsed_time(e) / 1e3)
+
+
+def fp64_ops_per_node(key: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_ops.json")) as fh:
+            d = json.load(fh)
+        return d.get(key), d.get("source")
+    except Exception:
+        return None, None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -284,6 +309,16 @@ def run_ours(args):
                "h2d_bytes_per_step": 8 * total_cells, "d2h_bytes_per_step": 8 * total_cells,
                "api": "ode_cfl_3(lax_friedrichs_rhs(g), ..., ScalarField(host), single_step) per step"}
 
+    # the binding roofline: FP64 pipe -- ops/node from the committed ncu count
+    fp64 = None
+    ops, src = fp64_ops_per_node(f"air3d_weno5_{os.environ.get('HJ_STAGE_KERNEL', 'brick')}")
+    if world == 1:
+        peak64 = fp64_peak(dev, _lib.load())
+        fp64 = {"peak_ops_per_s": peak64, "peak_source": "measured: hj_fp64_probe DFMA chains, this run",
+                "ops_per_unit": ops, "ops_source": src}
+        if ops:
+            fp64["achieved_ops_per_s"] = value * ops
+            fp64["frac"] = value * ops / peak64
     if rank != 0:
         return 0
     cpu = None
@@ -302,6 +337,7 @@ def run_ours(args):
                      "kernel": "hj_stage fused WENO5+LF+RK stage",
                      "bytes_per_launch": bytes_per_launch,
                      "note": "fp64 WENO5 is FP64-pipe bound (SURVEY 0.4); see fp64 block"},
+        "fp64": fp64,
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,

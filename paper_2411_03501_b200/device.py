@@ -39,7 +39,14 @@ def to_dev(a) -> torch.Tensor:
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
-    return t.detach().cpu().numpy()
+    """Device tensor -> numpy.  Large fields land in pinned host memory (torch's
+    caching host allocator) so the copy is a direct DMA, not a staged one."""
+    t = t.detach()
+    if t.is_cuda and t.numel() * t.element_size() >= (1 << 20):
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t)
+        return out.numpy()
+    return t.cpu().numpy()
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

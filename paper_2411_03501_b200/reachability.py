@@ -197,7 +197,7 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
             except Exception as err:
                 raise RuntimeError(f"tube interval {k} failed: {err}") from err
             prev = res.y
-            v = ScalarField(dev.to_host(prev))
+            v = ScalarField._from_device(dev.to_host(prev))   # finiteness checked on the device
             snaps.append(v)
             times.append(t1)
             if progress is not None:

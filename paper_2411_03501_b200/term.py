@@ -235,7 +235,7 @@ def _term_fused(t: float, v: ScalarField, cfg: TermConfig, g: Grid) -> TermOutpu
     bound = step_bound(alphas, g)
     if bound == np.inf and s.nonfinite & _lib.FLAG_HAM_NONZERO:
         warn_zero_dissipation()
-    return TermOutput(delta=ScalarField(dev.to_host(delta)), step_bound=bound)
+    return TermOutput(delta=ScalarField._from_device(dev.to_host(delta)), step_bound=bound)
 
 
 def _term_bridge(t: float, v: ScalarField, cfg: TermConfig, g: Grid) -> TermOutput:
