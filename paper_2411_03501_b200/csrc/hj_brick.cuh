@@ -51,7 +51,7 @@ __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) *
 template <int SCHEME, class Load, class Emit>
 __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line(ld, n, weno_divisors(sp.h), emit);
+    weno5_line<1>(ld, n, weno_divisors(sp.h), emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {
@@ -110,7 +110,6 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   {
     const int y = t / BYX, x = t % BYX;
     if (y0 + y < n1 && x0 + x < n2) {
-      const int nvalid = min(BZ, n0 - z0);
       const double* col = &S.v[(y + HB) * SVP + (x + HB)];
       const double* zlo = &S.zh[HB * BYX * BYX + y * BYX + x];          // plane k+3, k in [-3,-1]
       const double* zhi = &S.zh[(HB - BZ) * BYX * BYX + y * BYX + x];   // plane k-BZ+3, k >= BZ
@@ -122,7 +121,6 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
         return zhi[k * (BYX * BYX)];
       };
       auto emit = [&](int i, double L, double R) {
-        if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
         const int s = s00 + i * (BYX * BYX);
         S.p0[s] = 0.5 * (L + R);                               // term.py:101
         S.d[s] = 0.0 + ah * (R - L);                           // term.py:84-86 (from zeros)
@@ -134,13 +132,11 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   // ---- axis 1: thread (z, seg, x) walks SEG nodes along y
   {
     const int x = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-    const int nvalid = (z0 + z < n0 && x0 + x < n2) ? min(SEG, n1 - (y0 + seg * SEG)) : 0;
     const double* line = &S.v[z * PLANE + (HB + seg * SEG) * SVP + (x + HB)];
     const double ah = P.alpha_half[1];
     const int ybase = seg * SEG;
     auto ld = [&](int k) -> double { return line[k * SVP]; };
     auto emit = [&](int i, double L, double R) {
-      if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
       const int s = swz(z, ybase + i, x);
       S.p1[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
@@ -151,13 +147,11 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   // ---- axis 2: thread (z, seg, y) walks SEG nodes along x
   {
     const int y = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-    const int nvalid = (z0 + z < n0 && y0 + y < n1) ? min(SEG, n2 - (x0 + seg * SEG)) : 0;
     const double* line = &S.v[z * PLANE + (y + HB) * SVP + (HB + seg * SEG)];
     const double ah = P.alpha_half[2];
     const int row = (z * BYX + y) * BYX, xbase = seg * SEG;
     auto ld = [&](int k) -> double { return line[k]; };
     auto emit = [&](int i, double L, double R) {
-      if (i < nvalid && (!finite(L) || !finite(R))) flags |= HJ_NF_DERIV;
       const int s = row + ((xbase + i) ^ y);
       S.p2[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
@@ -182,6 +176,11 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
       p[0] = S.p0[s];
       p[1] = S.p1[s];
       p[2] = S.p2[s];
+      // derivative / p_avg finiteness, as ScalarField(p_avg) checks it (term.py:101):
+      // a non-finite one-sided derivative always makes its p_avg non-finite
+      if (((abs_hi(p[0]) | 0x000FFFFFu) >= 0x7FFFFFFFu) || ((abs_hi(p[1]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ||
+          ((abs_hi(p[2]) | 0x000FFFFFu) >= 0x7FFFFFFFu))
+        flags |= HJ_NF_DERIV;
       const int ix[3] = {gz, gy, gx};
       const double H = hamiltonian<HAM, 3>(P.ham, G.nodes, ix, p);
       if (!finite(H)) flags |= HJ_NF_HAM;
