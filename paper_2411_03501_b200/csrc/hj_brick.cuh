@@ -61,21 +61,112 @@ __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& 
   }
 }
 
+struct BrickCoord {
+  int z0, y0, x0, b;
+};
+
+__device__ __forceinline__ BrickCoord brick_coord(const GridArgs& G, int lin) {
+  const int nbx = (G.n[2] + BYX - 1) / BYX, nby = (G.n[1] + BYX - 1) / BYX, nbz = (G.n[0] + BZ - 1) / BZ;
+  BrickCoord c;
+  c.x0 = (lin % nbx) * BYX;
+  lin /= nbx;
+  c.y0 = (lin % nby) * BYX;
+  lin /= nby;
+  c.z0 = (lin % nbz) * BZ;
+  c.b = lin / nbz;
+  return c;
+}
+
+// L2 prefetch of a brick's rows (its planes with axis-1 halo rows, and the
+// axis-0 halo planes), issued while the current brick computes
+__device__ __forceinline__ void prefetch_brick(const GridArgs& G, const double* vin0, const BrickCoord& c, int t) {
+  const long long s0 = G.stride[0], s1 = G.stride[1];
+  for (int r = t; r < (BZ + 2 * HB) * SVR; r += BRICK_THREADS) {
+    const int z = r / SVR - HB, yy = r % SVR - HB;
+    const int gz = c.z0 + z, gy = c.y0 + yy;
+    if (gz < 0 || gz >= G.n[0] || gy < 0 || gy >= G.n[1]) continue;
+    const int gx = max(c.x0 - HB, 0);
+    const double* p = vin0 + (long long)c.b * G.batch_stride + gz * s0 + gy * s1 + gx;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
+  }
+}
+
 template <int SCHEME, int HAM, int MINB>
-__global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P) {
+__device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, const BrickCoord c, unsigned& flags,
+                                            const BrickCoord* next);
+
+template <int SCHEME, int HAM, int MINB>
+__global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P, int nbricks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(smem_raw);
+  unsigned flags = 0u;
+  // persistent CTAs: bricks blockIdx.x, +gridDim.x, ... (neighbouring CTAs take
+  // neighbouring bricks, so halo rows are shared through L2)
+  for (int lin = blockIdx.x; lin < nbricks; lin += gridDim.x) {
+    const BrickCoord c = brick_coord(P.g, lin);
+    const int nxt = lin + gridDim.x;
+    BrickCoord cn;
+    if (nxt < nbricks) cn = brick_coord(P.g, nxt);
+    stage_brick<SCHEME, HAM, MINB>(P, S, c, flags, nxt < nbricks ? &cn : nullptr);
+    __syncthreads();   // shared memory is reused by the next brick
+  }
+  if (P.stats) {
+    long long dummy[1] = {0};
+    reduce_stats<1>(P.stats, flags, P.tag, false, dummy, dummy);
+  }
+}
+
+template <int SCHEME, int HAM, int MINB>
+__device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, const BrickCoord c, unsigned& flags,
+                                            const BrickCoord* next) {
   const GridArgs& G = P.g;
   const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
-  const int nbz = (n0 + BZ - 1) / BZ;
-  const int bz = blockIdx.z % nbz, b = blockIdx.z / nbz;
-  const int z0 = bz * BZ, y0 = blockIdx.y * BYX, x0 = blockIdx.x * BYX;
-  const long long base = (long long)b * G.batch_stride;
+  const int z0 = c.z0, y0 = c.y0, x0 = c.x0;
+  const long long base = (long long)c.b * G.batch_stride;
   const double* __restrict__ vin = P.y_in + base;
   const long long s0 = G.stride[0], s1 = G.stride[1];
   const int t = threadIdx.x;
-  unsigned flags = 0u;
 
+  const bool zin = (z0 >= HB || G.ax[0].halo_lo) && (z0 + BZ + HB <= n0 || G.ax[0].halo_hi);
+  const bool interior = zin && z0 + BZ <= n0 && y0 >= HB && y0 + BYX + HB <= n1 && x0 >= HB && x0 + BYX + HB <= n2;
+  if (interior) {
+    // ---- load, interior brick: every value is in memory; all loads first
+    // in chunks of 8 loads in flight per thread (bounded register use)
+    constexpr int NV = (BZ * SVR * SVR + BRICK_THREADS - 1) / BRICK_THREADS;   // 16
+    constexpr int NZ = (2 * HB * BYX * BYX) / BRICK_THREADS;                  // 6
+    const double* vbase = vin + (z0 * s0 + (y0 - HB) * s1 + (x0 - HB));
+#pragma unroll 1
+    for (int j0 = 0; j0 < NV; j0 += 8) {
+      double vb[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = t + (j0 + j) * BRICK_THREADS;
+        const int z = q / (SVR * SVR), r = q % (SVR * SVR);
+        const int yy = r / SVR, xx = r % SVR;
+        const bool use = q < BZ * SVR * SVR && ((yy >= HB && yy < HB + BYX) || (xx >= HB && xx < HB + BYX));
+        vb[j] = use ? vbase[z * s0 + yy * s1 + xx] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = t + (j0 + j) * BRICK_THREADS;
+        if (q < BZ * SVR * SVR) {
+          const int z = q / (SVR * SVR), r = q % (SVR * SVR);
+          S.v[z * PLANE + (r / SVR) * SVP + (r % SVR)] = vb[j];
+        }
+      }
+    }
+    double zb[NZ];
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) {
+      const int q = t + j * BRICK_THREADS;
+      const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
+      const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+      zb[j] = vin[e * s0 + (y0 + yx / BYX) * s1 + (x0 + yx % BYX)];
+    }
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) S.zh[t + j * BRICK_THREADS] = zb[j];
+  } else {
   // ---- load: brick planes with axis-1/axis-2 halos (corners unused)
   for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
     const int z = q / (SVR * SVR), r = q % (SVR * SVR);
@@ -104,7 +195,9 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
     if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, G.ax[0], e);
     S.zh[q] = val;
   }
+  }  // boundary-brick load
   __syncthreads();
+  if (next) prefetch_brick(G, P.y_in, *next, t);
 
   // ---- axis 0: thread (y, x) walks its column (zh planes below / above)
   {
@@ -202,10 +295,6 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
       out[off] = o;
     }
   }
-  if (P.stats) {
-    long long dummy[1] = {0};
-    reduce_stats<1>(P.stats, flags, P.tag, false, dummy, dummy);
-  }
 }
 
 template <int SCHEME, int HAM, int MINB>
@@ -221,8 +310,13 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
     if (dev >= 0 && dev < 64) configured[dev] = true;
   }
   const GridArgs& G = P.g;
-  dim3 grid((G.n[2] + BYX - 1) / BYX, (G.n[1] + BYX - 1) / BYX, ((G.n[0] + BZ - 1) / BZ) * G.batch);
-  k_stage_brick<SCHEME, HAM, MINB><<<grid, BRICK_THREADS, smem, s>>>(P);
+  const long long nbricks = (long long)((G.n[2] + BYX - 1) / BYX) * ((G.n[1] + BYX - 1) / BYX) *
+                            ((G.n[0] + BZ - 1) / BZ) * G.batch;
+  static int sms[64] = {};
+  if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
+  const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
+  k_stage_brick<SCHEME, HAM, MINB><<<(unsigned)ctas, BRICK_THREADS, smem, s>>>(P, (int)nbricks);
   return cudaGetLastError();
 }
 
