@@ -48,10 +48,12 @@ struct BrickSmem {
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
-template <int SCHEME, class Load, class Emit>
+// UNR: unroll of the WENO walk (the window rotates with period 4; unrolling
+// by 4 removes the register moves at the price of registers)
+template <int SCHEME, int UNR = 1, class Load, class Emit>
 __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line<1>(ld, n, weno_divisors(sp.h), emit);
+    weno5_line<UNR>(ld, n, weno_divisors(sp.h), emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
 template <int SCHEME, int HAM, int MINB>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, const BrickCoord c, unsigned& flags,
                                             const BrickCoord* next) {
+  constexpr int WALK_UNROLL = (MINB == 1) ? 4 : 1;   // 1 CTA/SM variant: registers to spare
   const GridArgs& G = P.g;
   const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
   const int z0 = c.z0, y0 = c.y0, x0 = c.x0;
@@ -218,7 +221,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
         S.p0[s] = 0.5 * (L + R);                               // term.py:101
         S.d[s] = 0.0 + ah * (R - L);                           // term.py:84-86 (from zeros)
       };
-      line_walk<SCHEME>(ld, BZ, G.sp[0], emit);
+      line_walk<SCHEME, WALK_UNROLL>(ld, BZ, G.sp[0], emit);
     }
   }
   __syncthreads();
@@ -234,7 +237,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       S.p1[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
     };
-    line_walk<SCHEME>(ld, SEG, G.sp[1], emit);
+    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[1], emit);
   }
   __syncthreads();
   // ---- axis 2: thread (z, seg, y) walks SEG nodes along x
@@ -249,7 +252,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       S.p2[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
     };
-    line_walk<SCHEME>(ld, SEG, G.sp[2], emit);
+    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[2], emit);
   }
   __syncthreads();
 
