@@ -213,9 +213,14 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()   # (ranks may share a GPU in the gloo path check)
     torch.cuda.set_device(local)
+    backend = os.environ.get("HJ_DIST_BACKEND", "nccl")   # gloo only for 1-GPU path checks
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     n = args.n
     cfg = hj.air3d_term_config(scheme="weno5")
@@ -269,7 +274,7 @@ def run_ours(args):
     ms = start.elapsed_time(end)
     stage_ms = [a.elapsed_time(b) for a, b in ev_stage]
     if world > 1:
-        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     total_cells = cells_local * world

@@ -90,11 +90,24 @@ class TorchDistTransport:
         import torch.distributed as dist
 
         sends, recvs = halo_plan(self.slab)
-        ops = [dist.P2POp(dist.isend, buf[a:b], peer, self.group) for peer, (a, b) in sends]
-        ops += [dist.P2POp(dist.irecv, buf[a:b], peer, self.group) for peer, (a, b) in recvs]
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        if not sends and not recvs:
+            return
+        staged = buf.is_cuda and dist.get_backend(self.group) != "nccl"
+        if staged:
+            # gloo moves host tensors only: stage the halo planes through the host
+            torch.cuda.current_stream().synchronize()
+            sbufs = [buf[a:b].cpu() for _, (a, b) in sends]
+            rbufs = [torch.empty_like(buf[a:b], device="cpu") for _, (a, b) in recvs]
+        else:
+            sbufs = [buf[a:b] for _, (a, b) in sends]
+            rbufs = [buf[a:b] for _, (a, b) in recvs]
+        ops = [dist.P2POp(dist.isend, t, peer, self.group) for (peer, _), t in zip(sends, sbufs)]
+        ops += [dist.P2POp(dist.irecv, t, peer, self.group) for (peer, _), t in zip(recvs, rbufs)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        if staged:
+            for (_, (a, b)), t in zip(recvs, rbufs):
+                buf[a:b].copy_(t)
 
     def max_flags(self, flags: int) -> int:
         import torch.distributed as dist
