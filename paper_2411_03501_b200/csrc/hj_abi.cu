@@ -89,6 +89,7 @@ static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G, unsigned gh
     A.bcv = g->bc_value[a];
     A.halo_lo = (a == 0) ? g->halo_lo : 0;
     A.halo_hi = (a == 0) ? g->halo_hi : 0;
+    A.halo_n = (a == 0 && (g->halo_lo || g->halo_hi)) ? g->halo : 0;
     if (A.bc < HJ_BC_PERIODIC || A.bc > HJ_BC_DIRICHLET)
       return fail(HJ_EINVAL, "axis %d: unknown boundary kind %d", a, A.bc);
     if (((ghost_axes >> a) & 1u) && (A.halo_lo || A.halo_hi) && g->halo < ghost_width)
