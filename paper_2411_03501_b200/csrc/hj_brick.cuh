@@ -53,7 +53,7 @@ __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) *
 template <int SCHEME, int UNR = 1, class Load, class Emit>
 __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line<UNR>(ld, n, weno_divisors(sp.h), emit);
+    weno5_line<UNR, SEG>(ld, n, weno_divisors(sp.h), emit);   // every brick walk has SEG == BZ nodes
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {

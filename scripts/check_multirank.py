@@ -29,14 +29,14 @@ from paper_2411_03501_b200.engine import FusedIntegrator  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--backend", default="gloo")
-    ap.add_argument("--n", type=int, default=61)
+    ap.add_argument("--planes", type=int, default=61)
     ap.add_argument("--steps", type=int, default=3)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % torch.cuda.device_count())
     dist.init_process_group(args.backend)
-    g = hj.air3d_grid((args.n * world, 40, 36))
+    g = hj.air3d_grid((args.planes * world, 40, 36))
     cfg = hj.air3d_term_config(scheme="weno5")
     y0 = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0).values
     alphas = cfg.partials.alphas(0.0, g)
