@@ -184,6 +184,18 @@ int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alph
 int hj_eval_hamiltonian(const hj_grid* g, const hj_ham* ham, const double* const* p, double* out,
                         void* stream);
 
+/* The integration loop of ode_cfl_1/2/3 (integrator.py:69-126) natively:
+ * dt = cfl*bound, min(max_step) (max_step <= 0: none), clipped to the span,
+ * t = t1 on the last step; each TVD-RK stage one hj_stage launch (tags
+ * step*4 + stage), the mask applied in the final stage; no device sync.
+ * y_init is not written; buf0..2 are the work buffers (one of them, or
+ * y_init when no step is taken, is returned in *y_final).
+ * info (host, 6 doubles): t_final, steps, min_dt, max_dt, bad_dt_flag, bad_dt. */
+int hj_integrate(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, int order, double t0,
+                 double t1, double cfl, double max_step, int single_step, double bound, const double* y_init,
+                 double* buf0, double* buf1, double* buf2, const double* mask_prev, int mask, hj_stats* stats,
+                 double* info, double** y_final, void* stream);
+
 /* term_lax_friedrichs with a registered Hamiltonian: delta only (HJ_STAGE_DELTA). */
 int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha,
             const double* v, double* delta, hj_stats* stats, void* stream);

@@ -95,6 +95,9 @@ _SIGNATURES = [
     ("hj_count_below", c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     ("hj_stats_reset", c_int, [c_void_p, c_void_p]),
     ("hj_eval_hamiltonian", c_int, [POINTER(HjGrid), POINTER(HjHam), POINTER(c_void_p), c_void_p, c_void_p]),
+    ("hj_integrate", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_int, c_double, c_double,
+                             c_double, c_double, c_int, c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                             c_int, c_void_p, POINTER(c_double), POINTER(c_void_p), c_void_p]),
     ("hj_check_division", c_int, [c_int64, c_uint64, c_void_p, c_void_p]),
     ("hj_fp64_probe", c_int, [c_int, c_int, c_void_p, c_void_p]),
     ("hj_divided_differences", c_int, [POINTER(HjGrid), c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,

@@ -93,6 +93,8 @@ class FusedIntegrator:
             raise ValueError(f"tspan must be increasing, got [{t0}, {t1}]")
         kinds = _STAGES[order]
         mask = (_lib.MASK_MIN if use_min else _lib.MASK_MAX) if mask_prev is not None else _lib.MASK_NONE
+        if self._native_ok(opts):
+            return self._integrate_native(order, t0, t1, y, opts, mask_prev, mask, use_min, check)
         strm = dev.stream()
         self.stats.reset()
         bufs = self._buffers(y)
@@ -156,6 +158,73 @@ class FusedIntegrator:
         if check:
             self._raise_pending(times, warn=zero_alpha)
         return DeviceIntegration(t, cur, steps, min_dt, max_dt)
+
+    # ------------------------------------------------------------ native loop
+    def _native_ok(self, opts) -> bool:
+        """hj_integrate runs the whole loop in C++ when nothing needs the host
+        between stages: range-free bounds, no per-step stats printing, no
+        halo exchange (multi-GPU slabs override _stage)."""
+        return (self.range_free and not opts.collect_stats and self.exchange is None
+                and type(self)._stage is FusedIntegrator._stage)
+
+    def _integrate_native(self, order, t0, t1, y, opts, mask_prev, mask, use_min, check) -> DeviceIntegration:
+        import ctypes
+
+        alphas = self._alphas(t0, y)
+        bound = step_bound(alphas, self.g)
+        bufs = self._buffers(y)
+        info = (ctypes.c_double * 6)()
+        yfin = ctypes.c_void_p()
+        self.stats.reset()
+        rc = self.lib.hj_integrate(self.dg.ref, _lib.SCHEME_CODES[self.scheme], self.dh.ref,
+                                   _lib.doubles(alphas, _lib.HJ_MAX_DIM), int(order), t0, t1, float(opts.cfl_factor),
+                                   float(opts.max_step) if opts.max_step is not None else -1.0,
+                                   1 if opts.single_step else 0, float(bound), dev.ptr(y), dev.ptr(bufs[0]),
+                                   dev.ptr(bufs[1]), dev.ptr(bufs[2]), dev.ptr(mask_prev), int(mask), self.stats.p,
+                                   info, ctypes.byref(yfin), dev.stream())
+        _lib.check(rc, "hj_integrate")
+        t, steps, min_dt, max_dt = info[0], int(info[1]), info[2], info[3]
+        self.launches += steps * len(_STAGES[order])
+        if info[4]:
+            if check:
+                self._raise_pending(self._replay_times(order, t0, t1, bound, opts))
+            raise RuntimeError(f"step {steps}: no usable step size (dt={info[5]})")
+        if steps == 0:
+            cur = y.clone()
+            if mask_prev is not None:
+                dev.mask_dev(cur, mask_prev, use_min)
+        else:
+            cur = next(b for b in bufs if b.data_ptr() == yfin.value).clone()
+        if check:
+            self._raise_pending(self._replay_times(order, t0, t1, bound, opts), warn=bound == np.inf)
+        return DeviceIntegration(t, cur, steps, min_dt, max_dt)
+
+    @staticmethod
+    def _replay_times(order, t0, t1, bound, opts) -> dict[int, float]:
+        """Stage start times per tag, from the same scalar dt logic (only read
+        when an error has to be reported)."""
+
+        class _Lazy(dict):
+            def get(self, tag, default=None):
+                t, steps = t0, 0
+                while t < t1:
+                    dt = opts.cfl_factor * bound
+                    if opts.max_step is not None:
+                        dt = min(dt, opts.max_step)
+                    remaining = t1 - t
+                    last = dt >= remaining
+                    if last:
+                        dt = remaining
+                    if steps == tag // 4:
+                        k = tag % 4
+                        return (t, t + dt, t + 0.5 * dt)[k] if order == 3 else (t, t + dt)[min(k, 1)]
+                    t = t1 if last else t + dt
+                    steps += 1
+                    if opts.single_step:
+                        break
+                return default
+
+        return _Lazy()
 
     def step3(self, y: torch.Tensor, t: float, dt: float, events: list | None = None) -> torch.Tensor:
         """One TVD-RK3 step with a given dt on device state ``y`` (three fused
