@@ -2,6 +2,8 @@
 // include/hjb200.h).  Validation mirrors the reference's ValueError checks;
 // failures return HJ_E* and leave a thread-local message.
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -140,6 +142,29 @@ static int check_ham(const hj_ham* ham, int dim) {
   }
 }
 
+// Device scratch for the 4-D pre-pass, cached per (device, stream) so that
+// solvers on different streams never share it; grown on demand (cudaFree
+// synchronises, so a buffer is never released while in use).
+static double* scratch_for(cudaStream_t s, size_t n_doubles) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<double*, size_t>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = cache[{dev, s}];
+  if (e.second < n_doubles) {
+    if (e.first) cudaFree(e.first);
+    e = {nullptr, 0};
+    double* p = nullptr;
+    if (cudaMalloc((void**)&p, n_doubles * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;   // the caller falls back to the generic kernel
+    }
+    e = {p, n_doubles};
+  }
+  return e.first;
+}
+
 // Derived constants computed once on the host side of the ABI.
 static hj_ham prep_ham(const hj_ham* ham) {
   hj_ham h = *ham;
@@ -230,6 +255,15 @@ int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alph
   P.mask_prev = mask_prev;
   P.stats = stats;
   cudaStream_t s = (cudaStream_t)stream;
+  if (P.g.dim == 4) {
+    // 4-D brick path: scratch for the axis-0 pre-pass (p_avg0, d0)
+    const size_t span = (size_t)(P.g.batch_stride * (P.g.batch - 1) + P.g.cells);
+    double* scratch = scratch_for(s, 2 * span);
+    if (scratch) {
+      P.aux_p0 = scratch;
+      P.aux_d0 = scratch + span;
+    }
+  }
   bool handled = false;
   cudaError_t e = launch_stage_fast(scheme, P, s, &handled);
   if (!handled) e = launch_stage_generic(scheme, P, s);

@@ -1,23 +1,27 @@
-// hj_brick.cuh -- the fused LF + TVD-RK stage on 3-D grids, brick-tiled,
-// templated on the upwind scheme and the device Hamiltonian.
+// hj_brick.cuh -- the fused LF + TVD-RK stage, brick-tiled, templated on the
+// upwind scheme, the device Hamiltonian and the axis offset AO.
 //
-// One CTA (256 threads, ~110 KB shared memory, 2 CTAs per SM) owns an
-// 8 x 16 x 16 brick (axes 0, 1, 2).  Per stage and brick:
+// AO = 0 (3-D grids): one CTA (256 threads, ~110 KB shared memory, 2 CTAs per
+// SM, persistent over a brick sequence) owns an 8 x 16 x 16 brick of axes
+// (0, 1, 2).  Per stage and brick:
 //   load:   the brick's values, their axis-1/axis-2 halos and the 3+3 axis-0
 //           halo planes go to shared memory (coalesced; exchanged halo planes
 //           or boundary ghosts through fetch());
-//   axis 0: thread (y,x) walks its 8-node column, axis 1: thread (z,seg,x)
-//           walks 8 nodes along y, axis 2: thread (z,seg,y) walks 8 nodes
-//           along x -- every walk from shared memory through ONE inlined copy
-//           of the line walker (a runtime-configured loop over the axes);
-//           each stores p_avg_a = 0.5*(L+R) and accumulates the dissipation
+//   walks:  thread (y,x) walks its 8-node column along the brick's first
+//           axis, thread (z,seg,x) 8 nodes along its second, thread (z,seg,y)
+//           8 nodes along its third -- each from shared memory, storing
+//           p_avg_a = 0.5*(L+R) and accumulating the dissipation
 //           d = ((0 + d0) + d1) + d2, d_a = (alpha_a*0.5)*(R_a-L_a), in the
 //           reference's axis order (term.py:84-86);
 //   out:    per node, coalesced -- H(x, p_avg), delta = d - H (term.py:113),
 //           stage update (integrator.py:93-103), optional tube mask
 //           (reachability.py:249), non-finite flags, store.
-// The line walker (hj_weno_line.cuh / hj_eno_line.cuh) is a rolled loop with a
-// register window that computes every face quantity of its line once.
+// AO = 1 (4-D grids): the brick covers axes (1, 2, 3) of one axis-0 slice;
+// a pre-pass (k_axis0_walk) has already walked axis 0 and left p_avg0 and
+// d0 in scratch, so the first brick walk continues the dissipation from d0
+// and H receives four costates.
+// The line walkers (hj_weno_line.cuh / hj_eno_line.cuh) are rolled loops with
+// a register window that compute every face quantity of their line once.
 #pragma once
 #include "hj_eno_line.cuh"
 #include "hj_kernels.cuh"
@@ -25,35 +29,35 @@
 
 namespace hj {
 
-constexpr int BZ = 8;                  // brick depth along axis 0
-constexpr int BYX = 16;                // brick edge along axes 1 and 2
-constexpr int SEG = 8;                 // nodes per thread walk along axes 1 and 2
+constexpr int BZ = 8;                  // brick depth along its first axis
+constexpr int BYX = 16;                // brick edge along its other two axes
+constexpr int SEG = 8;                 // nodes per thread walk (all walks)
 constexpr int HB = 3;                  // ghost width held in shared memory (WENO5/ENO3 need 3)
 constexpr int SVP = BYX + 2 * HB + 1;  // 23: odd pitch (conflict-free LDS.64 across y-lanes)
 constexpr int SVR = BYX + 2 * HB;      // 22 rows per plane
 constexpr int PLANE = SVR * SVP;       // doubles per plane of v
 constexpr int NODES = BZ * BYX * BYX;  // 2048 nodes per brick
 constexpr int BRICK_THREADS = 256;
+static_assert(SEG == BZ, "the walks share one compile-time length");
 
 struct BrickSmem {
-  double v[BZ * PLANE];      // brick planes with axis-1 / axis-2 halos
-  double zh[2 * HB * BYX * BYX];  // axis-0 halo planes: 3 below, 3 above (interior y,x)
-  double p0[NODES];          // p_avg per axis (swizzled node index)
+  double v[BZ * PLANE];           // brick planes with halos of the second / third axis
+  double zh[2 * HB * BYX * BYX];  // first-axis halo planes: 3 below, 3 above (interior)
+  double p0[NODES];               // p_avg per brick axis (swizzled node index)
   double p1[NODES];
   double p2[NODES];
-  double d[NODES];           // running dissipation
+  double d[NODES];                // running dissipation
 };
 
 // node (z, y, x) of the brick -> slot in the per-node arrays; the XOR keeps
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
-// UNR: unroll of the WENO walk (the window rotates with period 4; unrolling
-// by 4 removes the register moves at the price of registers)
+// UNR: unroll of the WENO walk (the window rotates with period 4)
 template <int SCHEME, int UNR = 1, class Load, class Emit>
 __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line<UNR, SEG>(ld, n, weno_divisors(sp.h), emit);   // every brick walk has SEG == BZ nodes
+    weno5_line<UNR, SEG>(ld, n, weno_divisors(sp.h), emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {
@@ -63,12 +67,35 @@ __device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& 
   }
 }
 
+// The three grid axes a brick spans (AO, AO+1, AO+2) and its slice base.
+template <int AO>
+struct BrickView {
+  int n0, n1, n2;
+  long long s0, s1;
+  int slices;   // independent 3-D slices: batch (x n[0] when AO = 1)
+  __device__ __forceinline__ explicit BrickView(const GridArgs& G) {
+    n0 = G.n[AO];
+    n1 = G.n[AO + 1];
+    n2 = G.n[AO + 2];
+    s0 = G.stride[AO];
+    s1 = G.stride[AO + 1];
+    slices = AO ? G.batch * G.n[0] : G.batch;
+  }
+  // element offset of slice b from problem 0's first owned node
+  __device__ __forceinline__ long long slice_base(const GridArgs& G, int b) const {
+    if (AO == 0) return (long long)b * G.batch_stride;
+    const int pb = b / G.n[0], i0 = b % G.n[0];
+    return (long long)pb * G.batch_stride + (long long)i0 * G.stride[0];
+  }
+};
+
 struct BrickCoord {
   int z0, y0, x0, b;
 };
 
-__device__ __forceinline__ BrickCoord brick_coord(const GridArgs& G, int lin) {
-  const int nbx = (G.n[2] + BYX - 1) / BYX, nby = (G.n[1] + BYX - 1) / BYX, nbz = (G.n[0] + BZ - 1) / BZ;
+template <int AO>
+__device__ __forceinline__ BrickCoord brick_coord(const BrickView<AO>& V, int lin) {
+  const int nbx = (V.n2 + BYX - 1) / BYX, nby = (V.n1 + BYX - 1) / BYX, nbz = (V.n0 + BZ - 1) / BZ;
   BrickCoord c;
   c.x0 = (lin % nbx) * BYX;
   lin /= nbx;
@@ -79,38 +106,40 @@ __device__ __forceinline__ BrickCoord brick_coord(const GridArgs& G, int lin) {
   return c;
 }
 
-// L2 prefetch of a brick's rows (its planes with axis-1 halo rows, and the
-// axis-0 halo planes), issued while the current brick computes
-__device__ __forceinline__ void prefetch_brick(const GridArgs& G, const double* vin0, const BrickCoord& c, int t) {
-  const long long s0 = G.stride[0], s1 = G.stride[1];
+// L2 prefetch of a brick's rows, issued while the current brick computes
+template <int AO>
+__device__ __forceinline__ void prefetch_brick(const GridArgs& G, const BrickView<AO>& V, const double* vin0,
+                                               const BrickCoord& c, int t) {
+  const double* vb = vin0 + V.slice_base(G, c.b);
   for (int r = t; r < (BZ + 2 * HB) * SVR; r += BRICK_THREADS) {
     const int z = r / SVR - HB, yy = r % SVR - HB;
     const int gz = c.z0 + z, gy = c.y0 + yy;
-    if (gz < 0 || gz >= G.n[0] || gy < 0 || gy >= G.n[1]) continue;
+    if (gz < 0 || gz >= V.n0 || gy < 0 || gy >= V.n1) continue;
     const int gx = max(c.x0 - HB, 0);
-    const double* p = vin0 + (long long)c.b * G.batch_stride + gz * s0 + gy * s1 + gx;
+    const double* p = vb + gz * V.s0 + gy * V.s1 + gx;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
   }
 }
 
-template <int SCHEME, int HAM, int MINB>
-__device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, const BrickCoord c, unsigned& flags,
-                                            const BrickCoord* next);
+template <int SCHEME, int HAM, int MINB, int AO>
+__device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
+                                            const BrickCoord c, unsigned& flags, const BrickCoord* next);
 
-template <int SCHEME, int HAM, int MINB>
+template <int SCHEME, int HAM, int MINB, int AO>
 __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P, int nbricks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(smem_raw);
+  const BrickView<AO> V(P.g);
   unsigned flags = 0u;
   // persistent CTAs: bricks blockIdx.x, +gridDim.x, ... (neighbouring CTAs take
   // neighbouring bricks, so halo rows are shared through L2)
   for (int lin = blockIdx.x; lin < nbricks; lin += gridDim.x) {
-    const BrickCoord c = brick_coord(P.g, lin);
+    const BrickCoord c = brick_coord(V, lin);
     const int nxt = lin + gridDim.x;
     BrickCoord cn;
-    if (nxt < nbricks) cn = brick_coord(P.g, nxt);
-    stage_brick<SCHEME, HAM, MINB>(P, S, c, flags, nxt < nbricks ? &cn : nullptr);
+    if (nxt < nbricks) cn = brick_coord(V, nxt);
+    stage_brick<SCHEME, HAM, MINB, AO>(P, V, S, c, flags, nxt < nbricks ? &cn : nullptr);
     __syncthreads();   // shared memory is reused by the next brick
   }
   if (P.stats) {
@@ -119,23 +148,26 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   }
 }
 
-template <int SCHEME, int HAM, int MINB>
-__device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, const BrickCoord c, unsigned& flags,
-                                            const BrickCoord* next) {
+template <int SCHEME, int HAM, int MINB, int AO>
+__device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
+                                            const BrickCoord c, unsigned& flags, const BrickCoord* next) {
   constexpr int WALK_UNROLL = (MINB == 1) ? 4 : 1;   // 1 CTA/SM variant: registers to spare
   const GridArgs& G = P.g;
-  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
+  const AxisView& A0 = G.ax[AO];
+  const AxisView& A1 = G.ax[AO + 1];
+  const AxisView& A2 = G.ax[AO + 2];
+  const int n0 = V.n0, n1 = V.n1, n2 = V.n2;
   const int z0 = c.z0, y0 = c.y0, x0 = c.x0;
-  const long long base = (long long)c.b * G.batch_stride;
+  const long long base = V.slice_base(G, c.b);
   const double* __restrict__ vin = P.y_in + base;
-  const long long s0 = G.stride[0], s1 = G.stride[1];
+  const long long s0 = V.s0, s1 = V.s1;
   const int t = threadIdx.x;
 
-  const bool zin = (z0 >= HB || G.ax[0].halo_lo) && (z0 + BZ + HB <= n0 || G.ax[0].halo_hi);
+  const bool zin = (z0 >= HB || A0.halo_lo) && (z0 + BZ + HB <= n0 || A0.halo_hi);
   const bool interior = zin && z0 + BZ <= n0 && y0 >= HB && y0 + BYX + HB <= n1 && x0 >= HB && x0 + BYX + HB <= n2;
   if (interior) {
-    // ---- load, interior brick: every value is in memory; all loads first
-    // in chunks of 8 loads in flight per thread (bounded register use)
+    // ---- load, interior brick: every value is in memory; loads issued in
+    // chunks of 8 per thread before their shared-memory stores
     constexpr int NV = (BZ * SVR * SVR + BRICK_THREADS - 1) / BRICK_THREADS;   // 16
     constexpr int NZ = (2 * HB * BYX * BYX) / BRICK_THREADS;                  // 6
     const double* vbase = vin + (z0 * s0 + (y0 - HB) * s1 + (x0 - HB));
@@ -170,47 +202,50 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
 #pragma unroll
     for (int j = 0; j < NZ; ++j) S.zh[t + j * BRICK_THREADS] = zb[j];
   } else {
-  // ---- load: brick planes with axis-1/axis-2 halos (corners unused)
-  for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
-    const int z = q / (SVR * SVR), r = q % (SVR * SVR);
-    const int yy = r / SVR, xx = r % SVR;
-    const bool yin = yy >= HB && yy < HB + BYX, xin = xx >= HB && xx < HB + BYX;
-    if (!yin && !xin) continue;
-    const int gz = z0 + z, gy = y0 + yy - HB, gx = x0 + xx - HB;
-    double val = 0.0;
-    const bool gy_in = gy >= 0 && gy < n1, gx_in = gx >= 0 && gx < n2;
-    if (gz < n0) {
-      if (gy_in && gx_in) val = vin[gz * s0 + gy * s1 + gx];
-      else if (gx_in) val = fetch(vin + gz * s0 + gx, G.ax[1], gy);        // axis-1 ghost
-      else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, G.ax[2], gx);   // axis-2 ghost
-    } else if (gy_in && gx_in) {
-      val = fetch(vin + gy * s1 + gx, G.ax[0], gz);                         // axis-0 ghost (partial brick)
+    // ---- load, boundary brick: planes with second/third-axis halos (corners unused)
+    for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
+      const int z = q / (SVR * SVR), r = q % (SVR * SVR);
+      const int yy = r / SVR, xx = r % SVR;
+      const bool yin = yy >= HB && yy < HB + BYX, xin = xx >= HB && xx < HB + BYX;
+      if (!yin && !xin) continue;
+      const int gz = z0 + z, gy = y0 + yy - HB, gx = x0 + xx - HB;
+      double val = 0.0;
+      const bool gy_in = gy >= 0 && gy < n1, gx_in = gx >= 0 && gx < n2;
+      if (gz < n0) {
+        if (gy_in && gx_in) val = vin[gz * s0 + gy * s1 + gx];
+        else if (gx_in) val = fetch(vin + gz * s0 + gx, A1, gy);          // second-axis ghost
+        else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, A2, gx);     // third-axis ghost
+      } else if (gy_in && gx_in) {
+        val = fetch(vin + gy * s1 + gx, A0, gz);                           // first-axis ghost (partial brick)
+      }
+      S.v[z * PLANE + yy * SVP + xx] = val;
     }
-    S.v[z * PLANE + yy * SVP + xx] = val;
+    // first-axis halo planes (exchanged planes or boundary ghosts)
+    for (int q = t; q < 2 * HB * BYX * BYX; q += BRICK_THREADS) {
+      const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
+      const int y = yx / BYX, x = yx % BYX;
+      const int gy = y0 + y, gx = x0 + x;
+      const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+      double val = 0.0;
+      if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, A0, e);
+      S.zh[q] = val;
+    }
   }
-  // ---- load: axis-0 halo planes (exchanged planes or boundary ghosts)
-  for (int q = t; q < 2 * HB * BYX * BYX; q += BRICK_THREADS) {
-    const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
-    const int y = yx / BYX, x = yx % BYX;
-    const int gy = y0 + y, gx = x0 + x;
-    const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
-    double val = 0.0;
-    if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, G.ax[0], e);
-    S.zh[q] = val;
-  }
-  }  // boundary-brick load
   __syncthreads();
-  if (next) prefetch_brick(G, P.y_in, *next, t);
+  if (next) prefetch_brick<AO>(G, V, P.y_in, *next, t);
 
-  // ---- axis 0: thread (y, x) walks its column (zh planes below / above)
+  // ---- first brick axis: thread (y, x) walks its column (zh planes below / above)
   {
     const int y = t / BYX, x = t % BYX;
     if (y0 + y < n1 && x0 + x < n2) {
       const double* col = &S.v[(y + HB) * SVP + (x + HB)];
       const double* zlo = &S.zh[HB * BYX * BYX + y * BYX + x];          // plane k+3, k in [-3,-1]
       const double* zhi = &S.zh[(HB - BZ) * BYX * BYX + y * BYX + x];   // plane k-BZ+3, k >= BZ
-      const double ah = P.alpha_half[0];
+      const double ah = P.alpha_half[AO];
       const int s00 = swz(0, y, x);
+      // AO = 1: the dissipation continues from the axis-0 pre-pass (term.py:84-86 order)
+      const double* d0p = AO ? P.aux_d0 + base + z0 * s0 + (y0 + y) * s1 + (x0 + x) : nullptr;
+      const int zmax = n0 - z0;
       auto ld = [&](int k) -> double {
         if (k < 0) return zlo[k * (BYX * BYX)];
         if (k < BZ) return col[k * PLANE];
@@ -219,17 +254,18 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       auto emit = [&](int i, double L, double R) {
         const int s = s00 + i * (BYX * BYX);
         S.p0[s] = 0.5 * (L + R);                               // term.py:101
-        S.d[s] = 0.0 + ah * (R - L);                           // term.py:84-86 (from zeros)
+        const double prev = (AO && i < zmax) ? d0p[i * s0] : 0.0;
+        S.d[s] = prev + ah * (R - L);                          // term.py:84-86
       };
-      line_walk<SCHEME, WALK_UNROLL>(ld, BZ, G.sp[0], emit);
+      line_walk<SCHEME, WALK_UNROLL>(ld, BZ, G.sp[AO], emit);
     }
   }
   __syncthreads();
-  // ---- axis 1: thread (z, seg, x) walks SEG nodes along y
+  // ---- second brick axis: thread (z, seg, x) walks SEG nodes along y
   {
     const int x = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
     const double* line = &S.v[z * PLANE + (HB + seg * SEG) * SVP + (x + HB)];
-    const double ah = P.alpha_half[1];
+    const double ah = P.alpha_half[AO + 1];
     const int ybase = seg * SEG;
     auto ld = [&](int k) -> double { return line[k * SVP]; };
     auto emit = [&](int i, double L, double R) {
@@ -237,14 +273,14 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       S.p1[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
     };
-    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[1], emit);
+    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[AO + 1], emit);
   }
   __syncthreads();
-  // ---- axis 2: thread (z, seg, y) walks SEG nodes along x
+  // ---- third brick axis: thread (z, seg, y) walks SEG nodes along x
   {
     const int y = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
     const double* line = &S.v[z * PLANE + (y + HB) * SVP + (HB + seg * SEG)];
-    const double ah = P.alpha_half[2];
+    const double ah = P.alpha_half[AO + 2];
     const int row = (z * BYX + y) * BYX, xbase = seg * SEG;
     auto ld = [&](int k) -> double { return line[k]; };
     auto emit = [&](int i, double L, double R) {
@@ -252,15 +288,16 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       S.p2[s] = 0.5 * (L + R);
       S.d[s] = S.d[s] + ah * (R - L);
     };
-    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[2], emit);
+    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[AO + 2], emit);
   }
   __syncthreads();
 
-  // ---- per node: H, delta, stage update, mask, store (coalesced over axis 2)
+  // ---- per node: H, delta, stage update, mask, store (coalesced over the last axis)
   {
     const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
     const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
     double* __restrict__ out = P.y_out + base;
+    const int i0 = AO ? (c.b % G.n[0]) : 0;
 #pragma unroll 2
     for (int q = t; q < NODES; q += BRICK_THREADS) {
       const int z = q / (BYX * BYX), y = (q / BYX) % BYX, x = q % BYX;
@@ -268,17 +305,23 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
       if (gz >= n0 || gy >= n1 || gx >= n2) continue;
       const long long off = gz * s0 + gy * s1 + gx;
       const int s = swz(z, y, x);
-      double p[3];
-      p[0] = S.p0[s];
-      p[1] = S.p1[s];
-      p[2] = S.p2[s];
+      double p[3 + AO];
+      if (AO) p[0] = P.aux_p0[base + off];
+      p[AO] = S.p0[s];
+      p[AO + 1] = S.p1[s];
+      p[AO + 2] = S.p2[s];
       // derivative / p_avg finiteness, as ScalarField(p_avg) checks it (term.py:101):
       // a non-finite one-sided derivative always makes its p_avg non-finite
-      if (((abs_hi(p[0]) | 0x000FFFFFu) >= 0x7FFFFFFFu) || ((abs_hi(p[1]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ||
-          ((abs_hi(p[2]) | 0x000FFFFFu) >= 0x7FFFFFFFu))
-        flags |= HJ_NF_DERIV;
-      const int ix[3] = {gz, gy, gx};
-      const double H = hamiltonian<HAM, 3>(P.ham, G.nodes, ix, p);
+      unsigned nf = 0u;
+#pragma unroll
+      for (int a = 0; a < 3 + AO; ++a) nf |= ((abs_hi(p[a]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ? 1u : 0u;
+      if (nf) flags |= HJ_NF_DERIV;
+      int ix[3 + AO];
+      if (AO) ix[0] = i0;
+      ix[AO] = gz;
+      ix[AO + 1] = gy;
+      ix[AO + 2] = gx;
+      const double H = hamiltonian<HAM, 3 + AO>(P.ham, G.nodes, ix, p);
       if (!finite(H)) flags |= HJ_NF_HAM;
       if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
       const double delta = S.d[s] - H;                          // term.py:113
@@ -300,37 +343,80 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, BrickSmem& S, co
   }
 }
 
-template <int SCHEME, int HAM, int MINB>
+// ---- 4-D pre-pass: the axis-0 walks (one thread per column segment, coalesced
+// across the last axis); p_avg0 and d0 = 0 + (alpha0*0.5)*(R0-L0) to scratch
+template <int SCHEME>
+__global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
+  const GridArgs& G = P.g;
+  const long long plane = G.stride[0];
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= plane) return;
+  const int nseg = (G.n[0] + SEG - 1) / SEG;
+  const int seg = blockIdx.y % nseg, pb = blockIdx.y / nseg;
+  const int z0 = seg * SEG;
+  const long long base = (long long)pb * G.batch_stride + pos;
+  const double* col = P.y_in + base;
+  const AxisView A0 = G.ax[0];
+  const double ah = P.alpha_half[0];
+  const int zmax = G.n[0] - z0;
+  auto ld = [&](int k) -> double { return fetch(col, A0, z0 + k); };
+  auto emit = [&](int i, double L, double R) {
+    if (i < zmax) {
+      const long long o = base + (long long)(z0 + i) * plane;
+      P.aux_p0[o] = 0.5 * (L + R);                 // term.py:101
+      P.aux_d0[o] = 0.0 + ah * (R - L);            // term.py:84-86
+    }
+  };
+  line_walk<SCHEME, 1>(ld, SEG, G.sp[0], emit);
+}
+
+template <int SCHEME, int HAM, int MINB, int AO>
 static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const size_t smem = sizeof(BrickSmem);
   static bool configured[64] = {};  // per instantiation and device
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB, AO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = true;
   }
   const GridArgs& G = P.g;
-  const long long nbricks = (long long)((G.n[2] + BYX - 1) / BYX) * ((G.n[1] + BYX - 1) / BYX) *
-                            ((G.n[0] + BZ - 1) / BZ) * G.batch;
+  const long long slices = AO ? (long long)G.batch * G.n[0] : G.batch;
+  const long long nbricks = (long long)((G.n[AO + 2] + BYX - 1) / BYX) * ((G.n[AO + 1] + BYX - 1) / BYX) *
+                            ((G.n[AO] + BZ - 1) / BZ) * slices;
   static int sms[64] = {};
   if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
-  k_stage_brick<SCHEME, HAM, MINB><<<(unsigned)ctas, BRICK_THREADS, smem, s>>>(P, (int)nbricks);
+  if (AO) {
+    const long long plane = G.stride[0];
+    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(((G.n[0] + SEG - 1) / SEG) * G.batch));
+    k_axis0_walk<SCHEME><<<pg, 256, 0, s>>>(P);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_stage_brick<SCHEME, HAM, MINB, AO><<<(unsigned)ctas, BRICK_THREADS, smem, s>>>(P, (int)nbricks);
   return cudaGetLastError();
 }
 
 template <int SCHEME, int MINB>
 static cudaError_t launch_brick_ham(const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = true;
+  if (P.g.dim == 4) {
+    if (!P.aux_p0 || !P.aux_d0) { *handled = false; return cudaSuccess; }
+    switch (P.ham.kind) {
+      case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1>(P, s);
+      case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1>(P, s);
+      default: *handled = false; return cudaSuccess;
+    }
+  }
   switch (P.ham.kind) {
-    case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB>(P, s);
-    case HJ_HAM_ROCKETS: return launch_brick<SCHEME, HJ_HAM_ROCKETS, MINB>(P, s);
-    case HJ_HAM_ROCKETS_EXTREMAL: return launch_brick<SCHEME, HJ_HAM_ROCKETS_EXTREMAL, MINB>(P, s);
-    case HJ_HAM_AIR3D: return launch_brick<SCHEME, HJ_HAM_AIR3D, MINB>(P, s);
+    case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 0>(P, s);
+    case HJ_HAM_ROCKETS: return launch_brick<SCHEME, HJ_HAM_ROCKETS, MINB, 0>(P, s);
+    case HJ_HAM_ROCKETS_EXTREMAL: return launch_brick<SCHEME, HJ_HAM_ROCKETS_EXTREMAL, MINB, 0>(P, s);
+    case HJ_HAM_AIR3D: return launch_brick<SCHEME, HJ_HAM_AIR3D, MINB, 0>(P, s);
     default: *handled = false; return cudaSuccess;
   }
 }

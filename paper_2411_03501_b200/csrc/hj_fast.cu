@@ -27,9 +27,7 @@ static int stage_variant() {
 cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = false;
   const int variant = stage_variant();
-  if (variant == 0 || P.g.dim != 3 || P.want_ranges) return cudaSuccess;
-  const long long bz = (P.g.n[0] + 7) / 8, by = (P.g.n[1] + 15) / 16;
-  if (bz * (long long)P.g.batch > 65535 || by > 65535) return cudaSuccess;
+  if (variant == 0 || (P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return cudaSuccess;
   if (scheme == HJ_WENO5) return launch_brick_weno5(P, s, handled, variant);
   return launch_brick_eno(scheme, P, s, handled);
 }

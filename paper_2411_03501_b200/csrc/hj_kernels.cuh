@@ -34,6 +34,8 @@ struct StageArgs {
   double* y_out;
   const double* mask_prev;
   hj_stats* stats;
+  double* aux_p0;   // 4-D brick path: axis-0 p_avg and dissipation from the pre-pass
+  double* aux_d0;
 };
 
 // Split a linear owned-node index into (problem, per-axis indices) and the
