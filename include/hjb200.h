@@ -231,6 +231,11 @@ int hj_count_below(int64_t count, const double* v, double level,
 /* Self-check of the hoisted-reciprocal division used by the fast kernels:
  * n random/special operand pairs, *d_mismatch += #{div_by(a,b) != a/b} (bitwise). */
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);
+/* Stage-kernel family (A/B measurements and test coverage): 0 per-node generic
+ * kernel, 1 brick kernels when the grid has enough bricks (default), 2 brick
+ * WENO5 kernel at 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid; -1 reads
+ * HJ_STAGE_KERNEL from the environment.  Returns the previous setting. */
+int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
  * iters x 8 independent DFMA chains (time it with events on `stream`). */
 int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream);

@@ -100,6 +100,7 @@ _SIGNATURES = [
                              c_int, c_void_p, POINTER(c_double), POINTER(c_void_p), c_void_p]),
     ("hj_check_division", c_int, [c_int64, c_uint64, c_void_p, c_void_p]),
     ("hj_fp64_probe", c_int, [c_int, c_int, c_void_p, c_void_p]),
+    ("hj_set_stage_kernel", c_int, [c_int]),
     ("hj_divided_differences", c_int, [POINTER(HjGrid), c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p]),
 ]

@@ -3,7 +3,7 @@
 
 namespace hj {
 cudaError_t launch_brick_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int variant) {
-  if (variant == 2) return launch_brick_ham<HJ_WENO5, 1>(P, s, handled);
+  if (variant == 2) return launch_brick_ham<HJ_WENO5, 1>(P, s, handled);   // "brick1"
   return launch_brick_ham<HJ_WENO5, 2>(P, s, handled);
 }
 }  // namespace hj

@@ -11,15 +11,24 @@ cudaError_t launch_brick_eno(int scheme, const StageArgs& P, cudaStream_t s, boo
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
 //   "brick1"        : brick-tiled WENO5 kernel compiled for 1 CTA per SM
 //   "generic"       : per-node generic kernel everywhere
+static int g_variant = -1;   // -1: take HJ_STAGE_KERNEL from the environment
+
 static int stage_variant() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_variant < 0) {
     const char* e = std::getenv("HJ_STAGE_KERNEL");
-    v = 1;
+    int v = 1;
     if (e && std::string(e) == "generic") v = 0;
     if (e && std::string(e) == "brick1") v = 2;
+    if (e && std::string(e) == "brick_always") v = 3;   // brick kernels even on tiny grids
+    g_variant = v;
   }
-  return v;
+  return g_variant;
+}
+
+int set_stage_variant(int v) {
+  const int old = stage_variant();
+  g_variant = v;
+  return old;
 }
 
 // The brick kernels cover 3-D stages without range statistics whose grid
@@ -28,7 +37,25 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
   *handled = false;
   const int variant = stage_variant();
   if (variant == 0 || (P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return cudaSuccess;
+  // too few bricks to occupy the SMs (small grids such as C1's 51x51x36):
+  // the per-node kernel exposes more parallelism
+  const int ao = P.g.dim - 3;
+  const long long nbricks = (long long)((P.g.n[ao + 2] + 15) / 16) * ((P.g.n[ao + 1] + 15) / 16) *
+                            ((P.g.n[ao] + 7) / 8) * (ao ? (long long)P.g.n[0] : 1) * P.g.batch;
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  if (variant != 3 && nbricks < 2LL * nsm) return cudaSuccess;
   if (scheme == HJ_WENO5) return launch_brick_weno5(P, s, handled, variant);
   return launch_brick_eno(scheme, P, s, handled);
 }
 }  // namespace hj
+
+extern "C" int hj_set_stage_kernel(int variant) {
+  if (variant < -1 || variant > 3) return -1;
+  return hj::set_stage_variant(variant);
+}

@@ -23,6 +23,17 @@ def require():
     return _lib.load()
 
 
+STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3}
+
+
+def set_stage_kernel(name: str) -> str:
+    """Select the fused-stage kernel family (A/B runs, test coverage); returns the previous one."""
+    old = require().hj_set_stage_kernel(STAGE_KERNELS[name])
+    if old < 0:
+        raise ValueError(f"unknown stage kernel {name!r}")
+    return {v: k for k, v in STAGE_KERNELS.items()}[old]
+
+
 def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 

@@ -27,3 +27,15 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(params=["auto", "brick_always", "generic"])
+def stage_kernel(request):
+    """Run a GPU parity test under every fused-stage kernel family: the
+    default dispatch, the brick kernels forced even on tiny grids, and the
+    per-node generic kernel."""
+    from paper_2411_03501_b200 import device as dev
+
+    old = dev.set_stage_kernel(request.param)
+    yield request.param
+    dev.set_stage_kernel(old)

@@ -6,7 +6,7 @@ import pytest
 
 import paper_2411_03501_b200 as hj
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("stage_kernel")]
 
 
 @pytest.mark.parametrize("scheme", ["weno5", "eno2"])

@@ -12,7 +12,7 @@ from paper_2411_03501_b200 import device as dev
 from paper_2411_03501_b200.distributed import LocalTransport, SlabIntegrator, lockstep_step3, partition
 from paper_2411_03501_b200.engine import FusedIntegrator
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("stage_kernel")]
 
 
 def _run(g, cfg, y0_host, world, steps=3):

@@ -11,7 +11,7 @@ import paper_2411_03501_b200 as hj
 from golden_io import case_list, package_grid
 from pkg_configs import package_config
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("stage_kernel")]
 
 
 @pytest.mark.parametrize("meta,a", case_list("ghost.npz"))

@@ -18,7 +18,7 @@ from golden_io import spec_grid
 from hams import oracle_ham
 from oracle import hjoracle as orc
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("stage_kernel")]
 orc.set_threads(os.cpu_count() or 1)
 
 SPECS = [
