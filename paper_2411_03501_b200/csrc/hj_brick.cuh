@@ -298,7 +298,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
     const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
     double* __restrict__ out = P.y_out + base;
     const int i0 = AO ? (c.b % G.n[0]) : 0;
-#pragma unroll 2
+#pragma unroll   // all 8 nodes per thread: their global loads are in flight together
     for (int q = t; q < NODES; q += BRICK_THREADS) {
       const int z = q / (BYX * BYX), y = (q / BYX) % BYX, x = q % BYX;
       const int gz = z0 + z, gy = y0 + y, gx = x0 + x;
