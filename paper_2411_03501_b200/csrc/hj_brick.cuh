@@ -7,19 +7,22 @@
 //   load:   the brick's values, their axis-1/axis-2 halos and the 3+3 axis-0
 //           halo planes go to shared memory (coalesced; exchanged halo planes
 //           or boundary ghosts through fetch());
-//   walks:  thread (y,x) walks its 8-node column along the brick's first
-//           axis, thread (z,seg,x) 8 nodes along its second, thread (z,seg,y)
-//           8 nodes along its third -- each from shared memory, storing
-//           p_avg_a = 0.5*(L+R) and accumulating the dissipation
-//           d = ((0 + d0) + d1) + d2, d_a = (alpha_a*0.5)*(R_a-L_a), in the
-//           reference's axis order (term.py:84-86);
-//   out:    per node, coalesced -- H(x, p_avg), delta = d - H (term.py:113),
-//           stage update (integrator.py:93-103), optional tube mask
-//           (reachability.py:249), non-finite flags, store.
+//   walks:  warps 0-3 walk the 16-node lines along the brick's second axis,
+//           warps 4-7 those along its third (concurrently, one window fill
+//           per 16 nodes), storing p_avg_a = 0.5*(L+R) and the dissipation
+//           term d_a = (alpha_a*0.5)*(R_a-L_a) per node;
+//   fused:  thread (y,x) then walks its 8-node column along the first axis
+//           and, per node, sums d = ((0 + d_0) + d_1) + d_2 in the
+//           reference's axis order (term.py:84-86), evaluates H(x, p_avg),
+//           delta = d - H (term.py:113), the stage update
+//           (integrator.py:93-103), the optional tube mask
+//           (reachability.py:249), the non-finite flags, and stores the node
+//           (coalesced across x; its global stage inputs fetched one node
+//           ahead).
 // AO = 1 (4-D grids): the brick covers axes (1, 2, 3) of one axis-0 slice;
 // a pre-pass (k_axis0_walk) has already walked axis 0 and left p_avg0 and
-// d0 in scratch, so the first brick walk continues the dissipation from d0
-// and H receives four costates.
+// d0 in scratch, so the fused walk starts the dissipation sum from d0 and H
+// receives four costates.
 // The line walkers (hj_weno_line.cuh / hj_eno_line.cuh) are rolled loops with
 // a register window that compute every face quantity of their line once.
 #pragma once
@@ -31,22 +34,24 @@ namespace hj {
 
 constexpr int BZ = 8;                  // brick depth along its first axis
 constexpr int BYX = 16;                // brick edge along its other two axes
-constexpr int SEG = 8;                 // nodes per thread walk (all walks)
+constexpr int SEG = 8;                 // nodes per first-axis walk (= BZ)
+constexpr int LSEG = 16;               // nodes per second / third-axis walk (= BYX)
 constexpr int HB = 3;                  // ghost width held in shared memory (WENO5/ENO3 need 3)
 constexpr int SVP = BYX + 2 * HB + 1;  // 23: odd pitch (conflict-free LDS.64 across y-lanes)
 constexpr int SVR = BYX + 2 * HB;      // 22 rows per plane
 constexpr int PLANE = SVR * SVP;       // doubles per plane of v
 constexpr int NODES = BZ * BYX * BYX;  // 2048 nodes per brick
 constexpr int BRICK_THREADS = 256;
-static_assert(SEG == BZ, "the walks share one compile-time length");
+static_assert(SEG == BZ && LSEG == BYX, "each walk covers its whole brick edge");
+static_assert(BZ * BYX == BRICK_THREADS / 2, "half the CTA walks the second axis, half the third");
 
 struct BrickSmem {
   double v[BZ * PLANE];           // brick planes with halos of the second / third axis
   double zh[2 * HB * BYX * BYX];  // first-axis halo planes: 3 below, 3 above (interior)
-  double p0[NODES];               // p_avg per brick axis (swizzled node index)
-  double p1[NODES];
+  double p1[NODES];               // p_avg of the second / third brick axis (swizzled node index)
   double p2[NODES];
-  double d[NODES];                // running dissipation
+  double t1[NODES];               // dissipation terms (alpha_a*0.5)*(R_a-L_a) of those axes
+  double t2[NODES];
 };
 
 // node (z, y, x) of the brick -> slot in the per-node arrays; the XOR keeps
@@ -54,10 +59,11 @@ struct BrickSmem {
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
 // UNR: unroll of the WENO walk (the window rotates with period 4)
-template <int SCHEME, int UNR = 1, class Load, class Emit>
-__device__ __forceinline__ void line_walk(const Load& ld, int n, const Spacing& sp, const Emit& emit) {
+template <int SCHEME, int UNR, int N, class Load, class Emit>
+__device__ __forceinline__ void line_walk(const Load& ld, const Spacing& sp, const Emit& emit) {
+  constexpr int n = N;
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line<UNR, SEG>(ld, n, weno_divisors(sp.h), emit);
+    weno5_line<UNR, N>(ld, n, weno_divisors(sp.h), emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {
@@ -122,11 +128,11 @@ __device__ __forceinline__ void prefetch_brick(const GridArgs& G, const BrickVie
   }
 }
 
-template <int SCHEME, int HAM, int MINB, int AO>
+template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
                                             const BrickCoord c, unsigned& flags, const BrickCoord* next);
 
-template <int SCHEME, int HAM, int MINB, int AO>
+template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P, int nbricks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(smem_raw);
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
     const int nxt = lin + gridDim.x;
     BrickCoord cn;
     if (nxt < nbricks) cn = brick_coord(V, nxt);
-    stage_brick<SCHEME, HAM, MINB, AO>(P, V, S, c, flags, nxt < nbricks ? &cn : nullptr);
+    stage_brick<SCHEME, HAM, MINB, AO, UNR>(P, V, S, c, flags, nxt < nbricks ? &cn : nullptr);
     __syncthreads();   // shared memory is reused by the next brick
   }
   if (P.stats) {
@@ -148,10 +154,10 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
   }
 }
 
-template <int SCHEME, int HAM, int MINB, int AO>
+template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
                                             const BrickCoord c, unsigned& flags, const BrickCoord* next) {
-  constexpr int WALK_UNROLL = (MINB == 1) ? 4 : 1;   // 1 CTA/SM variant: registers to spare
+  constexpr int WALK_UNROLL = UNR;   // WENO walk unroll (removes window rotation moves)
   const GridArgs& G = P.g;
   const AxisView& A0 = G.ax[AO];
   const AxisView& A1 = G.ax[AO + 1];
@@ -234,7 +240,41 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   __syncthreads();
   if (next) prefetch_brick<AO>(G, V, P.y_in, *next, t);
 
-  // ---- first brick axis: thread (y, x) walks its column (zh planes below / above)
+  // ---- second and third brick axes together: warps 0-3 walk the BZ x BYX
+  // lines along y, warps 4-7 the lines along x, each a whole 16-node edge;
+  // they leave p_avg and the dissipation term of their axis per node
+  if (t < BRICK_THREADS / 2) {
+    const int x = t % BYX, z = t / BYX;
+    const double* line = &S.v[z * PLANE + HB * SVP + (x + HB)];
+    const double ah = P.alpha_half[AO + 1];
+    auto ld = [&](int k) -> double { return line[k * SVP]; };
+    auto emit = [&](int i, double L, double R) {
+      const int s = swz(z, i, x);
+      S.p1[s] = 0.5 * (L + R);                               // term.py:101
+      S.t1[s] = ah * (R - L);                                // term.py:85-86
+    };
+    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit);
+  } else {
+    const int y = t % BYX, z = (t - BRICK_THREADS / 2) / BYX;
+    const double* line = &S.v[z * PLANE + (y + HB) * SVP + HB];
+    const double ah = P.alpha_half[AO + 2];
+    const int row = (z * BYX + y) * BYX;
+    auto ld = [&](int k) -> double { return line[k]; };
+    auto emit = [&](int i, double L, double R) {
+      const int s = row + (i ^ y);
+      S.p2[s] = 0.5 * (L + R);
+      S.t2[s] = ah * (R - L);
+    };
+    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit);
+  }
+  __syncthreads();
+
+  // ---- first brick axis fused with the per-node update: thread (y, x) walks
+  // its column (zh planes below / above) and, per node, forms
+  //   d = ((prev + t_first) + t_second) + t_third     (term.py:84-86 axis order)
+  //   H(x, p_avg), delta = d - H (term.py:113), the stage update
+  //   (integrator.py:93-103), the optional tube mask (reachability.py:249),
+  // the non-finite flags, and stores the node (coalesced across x).
   {
     const int y = t / BYX, x = t % BYX;
     if (y0 + y < n1 && x0 + x < n2) {
@@ -243,102 +283,68 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       const double* zhi = &S.zh[(HB - BZ) * BYX * BYX + y * BYX + x];   // plane k-BZ+3, k >= BZ
       const double ah = P.alpha_half[AO];
       const int s00 = swz(0, y, x);
-      // AO = 1: the dissipation continues from the axis-0 pre-pass (term.py:84-86 order)
-      const double* d0p = AO ? P.aux_d0 + base + z0 * s0 + (y0 + y) * s1 + (x0 + x) : nullptr;
-      const int zmax = n0 - z0;
+      const int zmax = n0 - z0;   // nodes of this column inside the domain (may exceed BZ)
+      const long long off0 = (long long)z0 * s0 + (long long)(y0 + y) * s1 + (x0 + x);
+      const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
+      const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
+      double* __restrict__ out = P.y_out + base;
+      const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
+      const bool need_m = P.mask != HJ_MASK_NONE;
+      const int i0 = AO ? (c.b % G.n[0]) : 0;
+      // global inputs of the node being emitted, fetched one node ahead
+      double nz_y0 = 0.0, nz_m = 0.0, nz_p0 = 0.0, nz_d0 = 0.0;
+      auto fetch_node = [&](int i) {
+        const long long off = off0 + (long long)i * s0;
+        nz_y0 = need_y0 ? y0p[off] : 0.0;
+        nz_m = need_m ? mp[off] : 0.0;
+        if (AO) {
+          nz_p0 = P.aux_p0[base + off];
+          nz_d0 = P.aux_d0[base + off];
+        }
+      };
+      fetch_node(0);
       auto ld = [&](int k) -> double {
         if (k < 0) return zlo[k * (BYX * BYX)];
         if (k < BZ) return col[k * PLANE];
         return zhi[k * (BYX * BYX)];
       };
       auto emit = [&](int i, double L, double R) {
+        if (i >= zmax) return;
+        const double yz = nz_y0, pv = nz_m, a0 = nz_p0, d0 = nz_d0;
+        if (i + 1 < zmax && i + 1 < BZ) fetch_node(i + 1);
         const int s = s00 + i * (BYX * BYX);
-        S.p0[s] = 0.5 * (L + R);                               // term.py:101
-        const double prev = (AO && i < zmax) ? d0p[i * s0] : 0.0;
-        S.d[s] = prev + ah * (R - L);                          // term.py:84-86
-      };
-      line_walk<SCHEME, WALK_UNROLL>(ld, BZ, G.sp[AO], emit);
-    }
-  }
-  __syncthreads();
-  // ---- second brick axis: thread (z, seg, x) walks SEG nodes along y
-  {
-    const int x = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-    const double* line = &S.v[z * PLANE + (HB + seg * SEG) * SVP + (x + HB)];
-    const double ah = P.alpha_half[AO + 1];
-    const int ybase = seg * SEG;
-    auto ld = [&](int k) -> double { return line[k * SVP]; };
-    auto emit = [&](int i, double L, double R) {
-      const int s = swz(z, ybase + i, x);
-      S.p1[s] = 0.5 * (L + R);
-      S.d[s] = S.d[s] + ah * (R - L);
-    };
-    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[AO + 1], emit);
-  }
-  __syncthreads();
-  // ---- third brick axis: thread (z, seg, y) walks SEG nodes along x
-  {
-    const int y = t % BYX, seg = (t / BYX) % (BYX / SEG), z = t / (BYX * (BYX / SEG));
-    const double* line = &S.v[z * PLANE + (y + HB) * SVP + (HB + seg * SEG)];
-    const double ah = P.alpha_half[AO + 2];
-    const int row = (z * BYX + y) * BYX, xbase = seg * SEG;
-    auto ld = [&](int k) -> double { return line[k]; };
-    auto emit = [&](int i, double L, double R) {
-      const int s = row + ((xbase + i) ^ y);
-      S.p2[s] = 0.5 * (L + R);
-      S.d[s] = S.d[s] + ah * (R - L);
-    };
-    line_walk<SCHEME, WALK_UNROLL>(ld, SEG, G.sp[AO + 2], emit);
-  }
-  __syncthreads();
-
-  // ---- per node: H, delta, stage update, mask, store (coalesced over the last axis)
-  {
-    const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
-    const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
-    double* __restrict__ out = P.y_out + base;
-    const int i0 = AO ? (c.b % G.n[0]) : 0;
-#pragma unroll   // all 8 nodes per thread: their global loads are in flight together
-    for (int q = t; q < NODES; q += BRICK_THREADS) {
-      const int z = q / (BYX * BYX), y = (q / BYX) % BYX, x = q % BYX;
-      const int gz = z0 + z, gy = y0 + y, gx = x0 + x;
-      if (gz >= n0 || gy >= n1 || gx >= n2) continue;
-      const long long off = gz * s0 + gy * s1 + gx;
-      const int s = swz(z, y, x);
-      double p[3 + AO];
-      if (AO) p[0] = P.aux_p0[base + off];
-      p[AO] = S.p0[s];
-      p[AO + 1] = S.p1[s];
-      p[AO + 2] = S.p2[s];
-      // derivative / p_avg finiteness, as ScalarField(p_avg) checks it (term.py:101):
-      // a non-finite one-sided derivative always makes its p_avg non-finite
-      unsigned nf = 0u;
+        double p[3 + AO];
+        if (AO) p[0] = a0;
+        p[AO] = 0.5 * (L + R);                                   // term.py:101
+        p[AO + 1] = S.p1[s];
+        p[AO + 2] = S.p2[s];
+        // derivative / p_avg finiteness, as ScalarField(p_avg) checks it (term.py:101):
+        // a non-finite one-sided derivative always makes its p_avg non-finite
+        unsigned nf = 0u;
 #pragma unroll
-      for (int a = 0; a < 3 + AO; ++a) nf |= ((abs_hi(p[a]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ? 1u : 0u;
-      if (nf) flags |= HJ_NF_DERIV;
-      int ix[3 + AO];
-      if (AO) ix[0] = i0;
-      ix[AO] = gz;
-      ix[AO + 1] = gy;
-      ix[AO + 2] = gx;
-      const double H = hamiltonian<HAM, 3 + AO>(P.ham, G.nodes, ix, p);
-      if (!finite(H)) flags |= HJ_NF_HAM;
-      if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
-      const double delta = S.d[s] - H;                          // term.py:113
-      if (!finite(delta)) flags |= HJ_NF_DELTA;
-      const double yv = S.v[z * PLANE + (y + HB) * SVP + (x + HB)];
-      if (!finite(yv)) flags |= HJ_NF_INPUT;
-      const double yz = (P.stage >= HJ_STAGE_RK2_AVG) ? y0p[off] : 0.0;
-      double o = stage_update(P.stage, P.dt, yv, yz, delta);
-      if (P.mask == HJ_MASK_MIN) {
-        const double pv = mp[off];
-        o = (pv < o) ? pv : o;
-      } else if (P.mask == HJ_MASK_MAX) {
-        const double pv = mp[off];
-        o = (pv > o) ? pv : o;
-      }
-      if (!finite(o)) flags |= HJ_NF_OUTPUT;
-      out[off] = o;
+        for (int a = 0; a < 3 + AO; ++a) nf |= ((abs_hi(p[a]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ? 1u : 0u;
+        if (nf) flags |= HJ_NF_DERIV;
+        // AO = 1: the dissipation continues from the axis-0 pre-pass
+        const double dsum = (((AO ? d0 : 0.0) + ah * (R - L)) + S.t1[s]) + S.t2[s];
+        int ix[3 + AO];
+        if (AO) ix[0] = i0;
+        ix[AO] = z0 + i;
+        ix[AO + 1] = y0 + y;
+        ix[AO + 2] = x0 + x;
+        const double H = hamiltonian<HAM, 3 + AO>(P.ham, G.nodes, ix, p);
+        if (!finite(H)) flags |= HJ_NF_HAM;
+        if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
+        const double delta = dsum - H;                           // term.py:113
+        if (!finite(delta)) flags |= HJ_NF_DELTA;
+        const double yv = col[i * PLANE];
+        if (!finite(yv)) flags |= HJ_NF_INPUT;
+        double o = stage_update(P.stage, P.dt, yv, yz, delta);
+        if (P.mask == HJ_MASK_MIN) o = (pv < o) ? pv : o;
+        else if (P.mask == HJ_MASK_MAX) o = (pv > o) ? pv : o;
+        if (!finite(o)) flags |= HJ_NF_OUTPUT;
+        out[off0 + (long long)i * s0] = o;
+      };
+      line_walk<SCHEME, WALK_UNROLL, SEG>(ld, G.sp[AO], emit);
     }
   }
 }
@@ -367,17 +373,17 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
       P.aux_d0[o] = 0.0 + ah * (R - L);            // term.py:84-86
     }
   };
-  line_walk<SCHEME, 1>(ld, SEG, G.sp[0], emit);
+  line_walk<SCHEME, 1, SEG>(ld, G.sp[0], emit);
 }
 
-template <int SCHEME, int HAM, int MINB, int AO>
+template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const size_t smem = sizeof(BrickSmem);
   static bool configured[64] = {};  // per instantiation and device
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB, AO>,
+    cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB, AO, UNR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = true;
@@ -397,26 +403,26 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  k_stage_brick<SCHEME, HAM, MINB, AO><<<(unsigned)ctas, BRICK_THREADS, smem, s>>>(P, (int)nbricks);
+  k_stage_brick<SCHEME, HAM, MINB, AO, UNR><<<(unsigned)ctas, BRICK_THREADS, smem, s>>>(P, (int)nbricks);
   return cudaGetLastError();
 }
 
-template <int SCHEME, int MINB>
+template <int SCHEME, int MINB, int UNR = 1>
 static cudaError_t launch_brick_ham(const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = true;
   if (P.g.dim == 4) {
     if (!P.aux_p0 || !P.aux_d0) { *handled = false; return cudaSuccess; }
     switch (P.ham.kind) {
-      case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1>(P, s);
-      case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1>(P, s);
+      case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1, UNR>(P, s);
+      case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1, UNR>(P, s);
       default: *handled = false; return cudaSuccess;
     }
   }
   switch (P.ham.kind) {
-    case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 0>(P, s);
-    case HJ_HAM_ROCKETS: return launch_brick<SCHEME, HJ_HAM_ROCKETS, MINB, 0>(P, s);
-    case HJ_HAM_ROCKETS_EXTREMAL: return launch_brick<SCHEME, HJ_HAM_ROCKETS_EXTREMAL, MINB, 0>(P, s);
-    case HJ_HAM_AIR3D: return launch_brick<SCHEME, HJ_HAM_AIR3D, MINB, 0>(P, s);
+    case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 0, UNR>(P, s);
+    case HJ_HAM_ROCKETS: return launch_brick<SCHEME, HJ_HAM_ROCKETS, MINB, 0, UNR>(P, s);
+    case HJ_HAM_ROCKETS_EXTREMAL: return launch_brick<SCHEME, HJ_HAM_ROCKETS_EXTREMAL, MINB, 0, UNR>(P, s);
+    case HJ_HAM_AIR3D: return launch_brick<SCHEME, HJ_HAM_AIR3D, MINB, 0, UNR>(P, s);
     default: *handled = false; return cudaSuccess;
   }
 }

@@ -20,6 +20,7 @@ static int stage_variant() {
     if (e && std::string(e) == "generic") v = 0;
     if (e && std::string(e) == "brick1") v = 2;
     if (e && std::string(e) == "brick_always") v = 3;   // brick kernels even on tiny grids
+    if (e && std::string(e) == "brick_u2") v = 4;       // WENO5 walks unrolled by 2
     g_variant = v;
   }
   return g_variant;
@@ -56,6 +57,6 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 3) return -1;
+  if (variant < -1 || variant > 4) return -1;
   return hj::set_stage_variant(variant);
 }

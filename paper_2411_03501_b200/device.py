@@ -23,7 +23,7 @@ def require():
     return _lib.load()
 
 
-STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3}
+STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3, "brick_u2": 4}
 
 
 def set_stage_kernel(name: str) -> str:
