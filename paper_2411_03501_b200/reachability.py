@@ -5,7 +5,8 @@ interval, integrate the Lax-Friedrichs term with TVD-RK3, then mask against
 the previous snapshot (min for "over", max for "under").  With a registered
 device Hamiltonian the tube lives in HBM for the whole solve; every RK stage
 is one fused kernel and the mask is fused into the interval's last stage.
-Snapshots are copied to the host once per interval (they are the result).
+Snapshots are copied to the host once per interval (they are the result),
+on a side stream that overlaps the next interval's compute (SnapshotPipe).
 """
 from __future__ import annotations
 
@@ -14,6 +15,7 @@ from dataclasses import dataclass
 from typing import Callable, Sequence
 
 import numpy as np
+import torch
 
 from . import _lib
 from . import device as dev
@@ -169,6 +171,45 @@ class BRTResult:
     times: tuple[float, ...]
 
 
+class SnapshotPipe:
+    """Overlaps each interval's snapshot copy with the next interval's compute.
+
+    ``push`` queues a device->pinned-host copy of the interval's state on a
+    side stream (ordered after the interval's kernels by an event) and then
+    completes the PREVIOUS interval: waits for its copy, wraps it as a
+    ScalarField (finiteness was verified on the device) and calls ``progress``.
+    So interval k's copy runs while interval k+1's stages execute, and every
+    snapshot is handed out in order, before the solve moves two intervals on.
+    """
+
+    def __init__(self):
+        self.copy = torch.cuda.Stream()
+        self.pending = None
+
+    def push(self, k, t, state: torch.Tensor, snaps, times, progress) -> None:
+        host = torch.empty(state.shape, dtype=state.dtype, pin_memory=True)
+        self.copy.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.copy):
+            host.copy_(state, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.copy)
+        state.record_stream(self.copy)   # keep the tensor alive until the copy ran
+        self.drain(snaps, times, progress)
+        self.pending = (k, t, host, done)
+
+    def drain(self, snaps, times, progress) -> None:
+        if self.pending is None:
+            return
+        k, t, host, done = self.pending
+        self.pending = None
+        done.synchronize()
+        v = ScalarField._from_device(host.numpy())
+        snaps.append(v)
+        times.append(t)
+        if progress is not None:
+            progress(k, t, v)
+
+
 def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
                opts: IntegratorOptions | None = None,
                progress: Callable[[int, float, ScalarField], None] | None = None) -> BRTResult:
@@ -189,19 +230,21 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
 
         fi = FusedIntegrator(g, cfg)
         prev = dev.to_dev(target.values)
+        pipe = SnapshotPipe()
+        t0 = 0.0
         for k in range(1, global_steps + 1):
-            t0 = times[-1]
             t1 = horizon * k / global_steps
             try:
                 res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
             except Exception as err:
+                pipe.drain(snaps, times, progress)   # callbacks of the intervals that did finish
                 raise RuntimeError(f"tube interval {k} failed: {err}") from err
             prev = res.y
-            v = ScalarField._from_device(dev.to_host(prev))   # finiteness checked on the device
-            snaps.append(v)
-            times.append(t1)
-            if progress is not None:
-                progress(k, t1, v)
+            # interval k's snapshot streams to pinned host memory while
+            # interval k+1 computes; interval k-1's is handed out meanwhile
+            pipe.push(k, t1, prev, snaps, times, progress)
+            t0 = t1
+        pipe.drain(snaps, times, progress)
         return BRTResult(snapshots=tuple(snaps), times=tuple(times))
 
     from .integrator import ode_cfl_1, ode_cfl_2
