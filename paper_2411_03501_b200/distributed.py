@@ -236,3 +236,75 @@ def lockstep_step3(runs: list[SlabIntegrator], hub: LocalTransport, ys: list[tor
                        dev.stream())
         src = dst
     return src
+
+
+# ---------------------------------------------------------------- tube solve over slabs
+def gather_owned(slabs: list[Slab], owned: torch.Tensor, dst: int = 0, group=None) -> np.ndarray | None:
+    """Assemble the full field on rank ``dst`` from every rank's owned planes
+    (point-to-point, so slabs of unequal size need no padding).  NCCL moves
+    the device tensors directly; gloo stages them through the host.  Returns
+    the field on ``dst`` and None elsewhere."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank()
+    nccl = dist.get_backend(group) == "nccl"
+    mine = owned.contiguous() if (nccl or not owned.is_cuda) else owned.cpu()
+    if rank != dst:
+        dist.send(mine, dst, group=group)
+        return None
+    parts = []
+    for s in slabs:
+        if s.rank == dst:
+            parts.append(mine)
+            continue
+        buf = torch.empty((s.n,) + tuple(mine.shape[1:]), dtype=mine.dtype, device=mine.device)
+        dist.recv(buf, s.rank, group=group)
+        parts.append(buf)
+    full = torch.cat(parts, dim=0)
+    return dev.to_host(full) if full.is_cuda else full.numpy()
+
+
+def solve_tube_slabs(g, target, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3, opts=None,
+                     progress=None, group=None, halo: int | None = None, transport=None):
+    """solve_tube (reachability.solve_tube) with axis 0 split across the ranks
+    of a torch.distributed group: every rank integrates its slab (halo
+    exchange per stage, non-finite flags max-reduced per interval), masks
+    against its own previous slab, and per interval the owned planes are
+    gathered to rank 0, which collects the snapshots and calls ``progress``.
+    Rank 0 returns the BRTResult; the other ranks return one with the same
+    times and no snapshots.  Bit-identical to the single-GPU tube."""
+    import torch.distributed as dist
+
+    from .integrator import IntegratorOptions
+    from .reachability import BRTResult
+    from .spatial import GHOST_WIDTH
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    target_vals = np.asarray(target.values if hasattr(target, "values") else target, dtype=np.float64)
+    if horizon == 0:
+        return BRTResult(snapshots=(target,) if rank == 0 else (), times=(0.0,))
+    opts = opts or IntegratorOptions()
+    halo = halo if halo is not None else max(GHOST_WIDTH[cfg.derivative_scheme], 2)
+    si = SlabIntegrator(g, cfg, rank, world, halo=halo, transport=transport, group=group)
+    slabs = partition(g.counts[0], world, halo, g.is_periodic(0))
+    use_min = cfg.approximation_sign == "over"
+    prev = si.scatter(target_vals)
+    snaps = [target] if rank == 0 else []
+    times = [0.0]
+    for k in range(1, global_steps + 1):
+        t0, t1 = times[-1], horizon * k / global_steps
+        try:
+            res = si.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
+        except Exception as err:
+            raise RuntimeError(f"tube interval {k} failed: {err}") from err
+        prev = res.y
+        full = gather_owned(slabs, si.owned(prev), 0, group)
+        times.append(t1)
+        if rank == 0:
+            from .grid import ScalarField
+
+            v = ScalarField._from_device(full)
+            snaps.append(v)
+            if progress is not None:
+                progress(k, t1, v)
+    return BRTResult(snapshots=tuple(snaps), times=tuple(times))

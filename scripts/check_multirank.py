@@ -31,11 +31,16 @@ def main():
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--planes", type=int, default=61)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--tube", action="store_true",
+                    help="full tube solve (solve_tube_slabs, snapshots gathered to rank 0) vs solve_tube")
+    ap.add_argument("--scheme", default="weno5")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % torch.cuda.device_count())
     dist.init_process_group(args.backend)
+    if args.tube:
+        return tube(args, rank, world)
     g = hj.air3d_grid((args.planes * world, 40, 36))
     cfg = hj.air3d_term_config(scheme="weno5")
     y0 = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0).values
@@ -69,6 +74,27 @@ def main():
         print(f"multirank world={world} backend={args.backend}: bitwise_equal={ok}", flush=True)
         if not ok:
             sys.exit(1)
+    dist.destroy_process_group()
+
+
+def tube(args, rank, world):
+    from paper_2411_03501_b200.distributed import solve_tube_slabs
+
+    g = hj.air3d_grid((args.planes * world, 34, 30))
+    cfg = hj.air3d_term_config(scheme=args.scheme)
+    target = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0)
+    seen = []
+    res = solve_tube_slabs(g, target, cfg, 0.5, 3, order=3, progress=lambda k, t, v: seen.append(k))
+    if rank == 0:
+        ref = hj.solve_tube(g, target, cfg, 0.5, 3, order=3)
+        ok = tuple(res.times) == tuple(ref.times) and seen == [1, 2, 3] and len(res.snapshots) == 4
+        ok = ok and all(np.array_equal(a.values, b.values) for a, b in zip(res.snapshots, ref.snapshots))
+        print(f"multirank tube world={world} backend={args.backend} scheme={args.scheme}: bitwise_equal={ok}",
+              flush=True)
+        if not ok:
+            sys.exit(1)
+    else:
+        assert res.snapshots == () and len(res.times) == 4
     dist.destroy_process_group()
 
 

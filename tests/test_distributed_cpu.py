@@ -82,3 +82,32 @@ def test_gloo_halo_exchange(world, n0, periodic):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert list(out) == [1] * world
+
+
+def _gather_worker(rank, world, port, n0, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_03501_b200.distributed import gather_owned
+
+        full = np.random.default_rng(3).standard_normal((n0, 3, 4))
+        slabs = partition(n0, world, 3, False)
+        s = slabs[rank]
+        got = gather_owned(slabs, torch.from_numpy(full[s.lo:s.lo + s.n].copy()))
+        out[rank] = int(np.array_equal(got, full)) if rank == 0 else int(got is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n0", [(2, 13), (3, 20), (4, 17)])
+def test_gloo_gather_owned_uneven_slabs(world, n0):
+    ctx = mp.get_context("spawn")
+    out = ctx.Array("i", [0] * world)
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n0, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert list(out) == [1] * world
