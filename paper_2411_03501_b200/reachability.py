@@ -174,40 +174,63 @@ class BRTResult:
 class SnapshotPipe:
     """Overlaps each interval's snapshot copy with the next interval's compute.
 
-    ``push`` queues a device->pinned-host copy of the interval's state on a
-    side stream (ordered after the interval's kernels by an event) and then
-    completes the PREVIOUS interval: waits for its copy, wraps it as a
-    ScalarField (finiteness was verified on the device) and calls ``progress``.
-    So interval k's copy runs while interval k+1's stages execute, and every
-    snapshot is handed out in order, before the solve moves two intervals on.
+    ``push`` records an event after the interval's kernels and hands the
+    device->host copy to a worker thread, which waits for the event on a side
+    stream and copies into a fresh host array (pageable: a snapshot is a
+    retained result, and pinning fresh memory per snapshot costs more than
+    the copy -- scripts/d2h_probe.py); the main thread meanwhile launches the
+    next interval.  Then it completes the PREVIOUS interval: waits for its
+    copy and calls ``deliver(k, t, array)``.  Snapshots are delivered in
+    order, at most one interval behind the solve.  Small fields (C1's
+    0.75 MB) go through pinned staging on the side stream instead.
     """
 
-    def __init__(self):
+    def __init__(self, deliver):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.deliver = deliver
         self.copy = torch.cuda.Stream()
+        self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="hj-snapshot")
         self.pending = None
 
-    def push(self, k, t, state: torch.Tensor, snaps, times, progress) -> None:
-        host = torch.empty(state.shape, dtype=state.dtype, pin_memory=True)
-        self.copy.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(self.copy):
-            host.copy_(state, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self.copy)
-        state.record_stream(self.copy)   # keep the tensor alive until the copy ran
-        self.drain(snaps, times, progress)
-        self.pending = (k, t, host, done)
+    def _fetch(self, state: torch.Tensor, ready) -> np.ndarray:
+        with torch.cuda.device(state.device), torch.cuda.stream(self.copy):
+            self.copy.wait_event(ready)
+            out = np.empty(tuple(state.shape), dtype=np.float64)
+            torch.from_numpy(out).copy_(state)   # returns once the bytes are on the host
+        return out
 
-    def drain(self, snaps, times, progress) -> None:
+    SMALL = 4 << 20   # below this, pinned staging is cheap and a thread hand-off is not
+
+    def push(self, k, t, state: torch.Tensor) -> None:
+        if state.numel() * state.element_size() < self.SMALL:
+            host = torch.empty(state.shape, dtype=state.dtype, pin_memory=True)
+            self.copy.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self.copy):
+                host.copy_(state, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self.copy)
+            state.record_stream(self.copy)
+
+            def result():
+                done.synchronize()
+                return host.numpy()
+        else:
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream())
+            result = self.pool.submit(self._fetch, state, ready).result
+        self.drain()
+        self.pending = (k, t, result)
+
+    def drain(self) -> None:
         if self.pending is None:
             return
-        k, t, host, done = self.pending
+        k, t, result = self.pending
         self.pending = None
-        done.synchronize()
-        v = ScalarField._from_device(host.numpy())
-        snaps.append(v)
-        times.append(t)
-        if progress is not None:
-            progress(k, t, v)
+        self.deliver(k, t, result())
+
+    def close(self) -> None:
+        self.pool.shutdown(wait=True)
 
 
 def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
@@ -230,21 +253,32 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
 
         fi = FusedIntegrator(g, cfg)
         prev = dev.to_dev(target.values)
-        pipe = SnapshotPipe()
+
+        def deliver(k, t, values):
+            v = ScalarField._from_device(values)   # finiteness checked on the device
+            snaps.append(v)
+            times.append(t)
+            if progress is not None:
+                progress(k, t, v)
+
+        pipe = SnapshotPipe(deliver)
         t0 = 0.0
-        for k in range(1, global_steps + 1):
-            t1 = horizon * k / global_steps
-            try:
-                res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
-            except Exception as err:
-                pipe.drain(snaps, times, progress)   # callbacks of the intervals that did finish
-                raise RuntimeError(f"tube interval {k} failed: {err}") from err
-            prev = res.y
-            # interval k's snapshot streams to pinned host memory while
-            # interval k+1 computes; interval k-1's is handed out meanwhile
-            pipe.push(k, t1, prev, snaps, times, progress)
-            t0 = t1
-        pipe.drain(snaps, times, progress)
+        try:
+            for k in range(1, global_steps + 1):
+                t1 = horizon * k / global_steps
+                try:
+                    res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
+                except Exception as err:
+                    pipe.drain()   # callbacks of the intervals that did finish
+                    raise RuntimeError(f"tube interval {k} failed: {err}") from err
+                prev = res.y
+                # interval k's snapshot streams to the host while interval k+1
+                # computes; interval k-1's is handed out meanwhile
+                pipe.push(k, t1, prev)
+                t0 = t1
+            pipe.drain()
+        finally:
+            pipe.close()
         return BRTResult(snapshots=tuple(snaps), times=tuple(times))
 
     from .integrator import ode_cfl_1, ode_cfl_2
@@ -293,16 +327,23 @@ def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_s
     snaps = [tgt] if keep_snapshots else []
     times = [0.0]
     use_min = cfg.approximation_sign == "over"
-    for k in range(1, global_steps + 1):
-        t0, t1 = times[-1], horizon * k / global_steps
-        try:
-            res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
-        except Exception as err:
-            raise RuntimeError(f"tube interval {k} failed: {err}") from err
-        prev = res.y
-        if keep_snapshots:
-            snaps.append(dev.to_host(prev))
-        times.append(t1)
+    pipe = SnapshotPipe(lambda k, t, values: snaps.append(values)) if keep_snapshots else None
+    try:
+        for k in range(1, global_steps + 1):
+            t0, t1 = times[-1], horizon * k / global_steps
+            try:
+                res = fi.integrate(order, (t0, t1), prev, opts, mask_prev=prev, use_min=use_min)
+            except Exception as err:
+                raise RuntimeError(f"tube interval {k} failed: {err}") from err
+            prev = res.y
+            if pipe is not None:
+                pipe.push(k, t1, prev)
+            times.append(t1)
+        if pipe is not None:
+            pipe.drain()
+    finally:
+        if pipe is not None:
+            pipe.close()
     return (np.stack(snaps) if keep_snapshots else dev.to_host(prev)), tuple(times)
 
 

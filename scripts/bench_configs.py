@@ -33,12 +33,16 @@ from paper_2411_03501_b200 import device as dev  # noqa: E402
 from paper_2411_03501_b200.engine import FusedIntegrator  # noqa: E402
 
 
-def sync_time(fn):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    out = fn()
-    torch.cuda.synchronize()
-    return time.perf_counter() - t0, out
+def sync_time(fn, reps=1):
+    """median wall time of ``reps`` calls (synchronised), and the last result"""
+    secs = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        secs.append(time.perf_counter() - t0)
+    return float(np.median(secs)), out
 
 
 def c1():
@@ -46,7 +50,7 @@ def c1():
     cfg = hj.air3d_term_config(scheme="eno2")
     target = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0)
     hj.solve_tube(g, target, cfg, 0.35, 1, order=2)   # warm
-    secs, res = sync_time(lambda: hj.solve_tube(g, target, cfg, 2.8, 8, order=2))
+    secs, res = sync_time(lambda: hj.solve_tube(g, target, cfg, 2.8, 8, order=2), reps=5)
     fi = FusedIntegrator(g, cfg)
     steps = 0
     t = 0.0
@@ -63,7 +67,7 @@ def c1():
     snaps, _, _ = orc.solve_brt(g, oracle_ham("air3d", g), "eno2", target.values, 2.8, 8, order=2)
     cpu_secs = time.perf_counter() - t0
     same = all(np.array_equal(a.values, b) for a, b in zip(res.snapshots, snaps))
-    return {"config": "C1 Air3D 51x51x36 ENO2+LF+odeCFL2 t=[0,2.8] 8 intervals (full solve, public API)",
+    return {"config": "C1 Air3D 51x51x36 ENO2+LF+odeCFL2 t=[0,2.8] 8 intervals (full solve, public API, median of 5)",
             "gpu_seconds": secs, "rk_steps": steps, "stages": 2 * steps,
             "cell_updates_per_s": cells * 2 * steps / secs,
             "cpu_oracle_seconds": cpu_secs, "cpu_threads": os.cpu_count(),
@@ -121,11 +125,11 @@ def c2s():
     target = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0)
     horizon = 0.02
     hj.solve_tube(g, target, cfg, 0.002, 1)
-    secs, res = sync_time(lambda: hj.solve_tube(g, target, cfg, horizon, 4))
+    secs, res = sync_time(lambda: hj.solve_tube(g, target, cfg, horizon, 4), reps=3)
     alphas = cfg.partials.alphas(0.0, g)
     dt = 0.5 / float(np.sum(alphas / g.spacings))
     steps = sum(int(np.ceil((horizon / 4) / dt - 1e-12)) for _ in range(4))
-    return {"config": "C2 Air3D 301^3 WENO5 solve_tube, horizon 0.02 in 4 intervals (public API, snapshots to host)",
+    return {"config": "C2 Air3D 301^3 WENO5 solve_tube, horizon 0.02 in 4 intervals (public API, snapshots to host, median of 3)",
             "seconds": secs, "approx_rk3_steps": steps,
             "cell_updates_per_s": 301 ** 3 * 3 * steps / secs}
 
