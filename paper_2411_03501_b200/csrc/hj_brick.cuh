@@ -52,7 +52,11 @@ struct BrickSmem {
   double p2[NODES];
   double t1[NODES];               // dissipation terms (alpha_a*0.5)*(R_a-L_a) of those axes
   double t2[NODES];
+  // ham_eval inputs of the brick: node coordinates along its three axes
+  // [BZ | BYX | BYX], then the Hamiltonian's two tables along its third axis
+  double crd[BZ + 4 * BYX];
 };
+constexpr int CRD_Y = BZ, CRD_X = BZ + BYX, CRD_T0 = BZ + 2 * BYX, CRD_T1 = BZ + 3 * BYX;
 
 // node (z, y, x) of the brick -> slot in the per-node arrays; the XOR keeps
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
@@ -128,6 +132,16 @@ __device__ __forceinline__ void prefetch_brick(const GridArgs& G, const BrickVie
   }
 }
 
+// 8-byte global -> shared asynchronous copy (LDGSTS) and its completion wait
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
                                             const BrickCoord c, unsigned& flags, const BrickCoord* next);
@@ -172,41 +186,28 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   const bool zin = (z0 >= HB || A0.halo_lo) && (z0 + BZ + HB <= n0 || A0.halo_hi);
   const bool interior = zin && z0 + BZ <= n0 && y0 >= HB && y0 + BYX + HB <= n1 && x0 >= HB && x0 + BYX + HB <= n2;
   if (interior) {
-    // ---- load, interior brick: every value is in memory; loads issued in
-    // chunks of 8 per thread before their shared-memory stores
-    constexpr int NV = (BZ * SVR * SVR + BRICK_THREADS - 1) / BRICK_THREADS;   // 16
-    constexpr int NZ = (2 * HB * BYX * BYX) / BRICK_THREADS;                  // 6
+    // ---- load, interior brick: every value is in memory.  cp.async (8 B per
+    // element) puts all of the brick's loads in flight at once without
+    // staging them in registers; the plane corners (never read) are skipped.
+    const int lane = t & 31, warp = t >> 5;
     const double* vbase = vin + (z0 * s0 + (y0 - HB) * s1 + (x0 - HB));
-#pragma unroll 1
-    for (int j0 = 0; j0 < NV; j0 += 8) {
-      double vb[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int q = t + (j0 + j) * BRICK_THREADS;
-        const int z = q / (SVR * SVR), r = q % (SVR * SVR);
-        const int yy = r / SVR, xx = r % SVR;
-        const bool use = q < BZ * SVR * SVR && ((yy >= HB && yy < HB + BYX) || (xx >= HB && xx < HB + BYX));
-        vb[j] = use ? vbase[z * s0 + yy * s1 + xx] : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int q = t + (j0 + j) * BRICK_THREADS;
-        if (q < BZ * SVR * SVR) {
-          const int z = q / (SVR * SVR), r = q % (SVR * SVR);
-          S.v[z * PLANE + (r / SVR) * SVP + (r % SVR)] = vb[j];
-        }
-      }
+    const bool xin = lane >= HB && lane < HB + BYX;
+#pragma unroll 2
+    for (int row = warp; row < BZ * SVR; row += BRICK_THREADS / 32) {   // 22 rows per warp
+      const int z = row / SVR, yy = row % SVR;
+      const bool yin = yy >= HB && yy < HB + BYX;
+      if (lane < SVR && (yin || xin)) cp_async8(&S.v[z * PLANE + yy * SVP + lane], vbase + z * s0 + yy * s1 + lane);
     }
-    double zb[NZ];
+    // first-axis halo planes: 6 x 16 rows of 16, two rows per warp instruction
+    const int half = lane >> 4, xl = lane & (BYX - 1);
 #pragma unroll
-    for (int j = 0; j < NZ; ++j) {
-      const int q = t + j * BRICK_THREADS;
-      const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
+    for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
+      const int row = 2 * r2 + half;
+      const int k = row / BYX, y = row % BYX;
       const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
-      zb[j] = vin[e * s0 + (y0 + yx / BYX) * s1 + (x0 + yx % BYX)];
+      cp_async8(&S.zh[row * BYX + xl], vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
     }
-#pragma unroll
-    for (int j = 0; j < NZ; ++j) S.zh[t + j * BRICK_THREADS] = zb[j];
+    cp_async_wait_all();
   } else {
     // ---- load, boundary brick: planes with second/third-axis halos (corners unused)
     for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
@@ -236,6 +237,23 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, A0, e);
       S.zh[q] = val;
     }
+  }
+  // the Hamiltonian's node-table inputs for this brick (global loads once per
+  // brick instead of per node)
+  // (3-D only: the 4-D pair's inputs are constant along the fused walk)
+  if (AO == 0 && HAM != HJ_HAM_ADVECTION && t < BZ + 4 * BYX) {
+    double val = 0.0;
+    if (t < CRD_Y) {
+      if (z0 + t < n0) val = G.nodes[AO][z0 + t];
+    } else if (t < CRD_X) {
+      if (y0 + t - CRD_Y < n1) val = G.nodes[AO + 1][y0 + t - CRD_Y];
+    } else if (t < CRD_T0) {
+      if (x0 + t - CRD_X < n2) val = G.nodes[AO + 2][x0 + t - CRD_X];
+    } else {
+      const int w = (t - CRD_T0) / BYX, k = (t - CRD_T0) % BYX;
+      if (P.ham.tab[w] && x0 + k < n2) val = P.ham.tab[w][x0 + k];
+    }
+    S.crd[t] = val;
   }
   __syncthreads();
   if (next) prefetch_brick<AO>(G, V, P.y_in, *next, t);
@@ -290,7 +308,6 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       double* __restrict__ out = P.y_out + base;
       const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
       const bool need_m = P.mask != HJ_MASK_NONE;
-      const int i0 = AO ? (c.b % G.n[0]) : 0;
       // global inputs of the node being emitted, fetched one node ahead
       double nz_y0 = 0.0, nz_m = 0.0, nz_p0 = 0.0, nz_d0 = 0.0;
       auto fetch_node = [&](int i) {
@@ -326,12 +343,20 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         if (nf) flags |= HJ_NF_DERIV;
         // AO = 1: the dissipation continues from the axis-0 pre-pass
         const double dsum = (((AO ? d0 : 0.0) + ah * (R - L)) + S.t1[s]) + S.t2[s];
-        int ix[3 + AO];
-        if (AO) ix[0] = i0;
-        ix[AO] = z0 + i;
-        ix[AO + 1] = y0 + y;
-        ix[AO + 2] = x0 + x;
-        const double H = hamiltonian<HAM, 3 + AO>(P.ham, G.nodes, ix, p);
+        // ham_eval inputs (hj_ham.cuh): 3-D Hamiltonians take the axis-0/1 nodes
+        // and the axis-2 tables (staged per brick); the 4-D pair takes the
+        // axis-2/3 nodes, constant along this walk
+        double cin[4] = {0.0, 0.0, 0.0, 0.0};
+        if (AO == 0) {
+          cin[0] = S.crd[i];
+          cin[1] = S.crd[CRD_Y + y];
+          cin[2] = S.crd[CRD_T0 + x];
+          cin[3] = S.crd[CRD_T1 + x];
+        } else {
+          int ix[4] = {c.b % G.n[0], z0 + i, y0 + y, x0 + x};
+          ham_inputs<HAM, 4>(P.ham, G.nodes, ix, cin);
+        }
+        const double H = ham_eval<HAM, 3 + AO>(P.ham, cin, p);
         if (!finite(H)) flags |= HJ_NF_HAM;
         if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
         const double delta = dsum - H;                           // term.py:113
