@@ -44,8 +44,13 @@ enum {
 /* boundary kinds -- grid.py:26-52 (BoundaryCondition / periodic / extrapolate / dirichlet) */
 enum { HJ_BC_PERIODIC = 0, HJ_BC_EXTRAPOLATE = 1, HJ_BC_DIRICHLET = 2 };
 
-/* derivative schemes -- spatial.py:260-266 (_SCHEMES) */
-enum { HJ_FIRST = 0, HJ_ENO2 = 1, HJ_ENO3 = 2, HJ_WENO5 = 3 };
+/* derivative schemes -- spatial.py:260-266 (_SCHEMES).
+ * HJ_WENO5_FMA is an addition: the same WENO5 scheme evaluated in tolerance
+ * mode (FMA contraction, reciprocal multiplies, one division per side for the
+ * weights) -- not bit-exact, but within the north-star contract (L-inf
+ * relative <= 1e-9 of the reference over a solve, sign(V) preserved); every
+ * other scheme is bit-exact. */
+enum { HJ_FIRST = 0, HJ_ENO2 = 1, HJ_ENO3 = 2, HJ_WENO5 = 3, HJ_WENO5_FMA = 4 };
 
 /* WENO epsilon modes -- spatial.py:205-211 */
 enum { HJ_EPS_SQUARED = 0, HJ_EPS_RAW = 1 };

@@ -17,7 +17,7 @@ HJ_OK, HJ_EINVAL, HJ_ECUDA = 0, -1, -2
 # boundary kinds
 BC_CODES = {"periodic": 0, "extrapolate": 1, "dirichlet": 2}
 # schemes (spatial.py:260-266)
-SCHEME_CODES = {"first": 0, "eno2": 1, "eno3": 2, "weno5": 3}
+SCHEME_CODES = {"first": 0, "eno2": 1, "eno3": 2, "weno5": 3, "weno5_fma": 4}
 EPS_CODES = {"squared": 0, "raw": 1}
 # Hamiltonian kinds
 HAM_ADVECTION, HAM_ROCKETS, HAM_ROCKETS_EXTREMAL, HAM_AIR3D, HAM_DI4 = range(5)

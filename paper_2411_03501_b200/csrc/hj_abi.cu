@@ -104,6 +104,7 @@ static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G, unsigned gh
     G->sp[a].h = g->h[a];
     G->sp[a].h2 = 2.0 * g->h[a];
     G->sp[a].h3 = 3.0 * g->h[a];
+    G->sp[a].rh = 1.0 / g->h[a];
     G->nodes[a] = g->nodes[a];
   }
   return HJ_OK;
@@ -121,6 +122,7 @@ static int ghost_width_of(int scheme) {
     case HJ_ENO2: return 2;
     case HJ_ENO3: return 3;
     case HJ_WENO5: return 3;
+    case HJ_WENO5_FMA: return 3;
     default: return -1;
   }
 }

@@ -68,6 +68,8 @@ __device__ __forceinline__ void line_walk(const Load& ld, const Spacing& sp, con
   constexpr int n = N;
   if constexpr (SCHEME == HJ_WENO5) {
     weno5_line<UNR, N>(ld, n, weno_divisors(sp.h), emit);
+  } else if constexpr (SCHEME == HJ_WENO5_FMA) {
+    weno5_fma_line<UNR, N>(ld, n, sp.rh, emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
     eno3_line(ld, n, eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {

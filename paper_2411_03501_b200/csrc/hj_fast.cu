@@ -6,6 +6,7 @@
 namespace hj {
 cudaError_t launch_brick_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
 cudaError_t launch_brick_eno(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
+cudaError_t launch_brick_weno5_fma(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
 
 // HJ_STAGE_KERNEL selects the stage kernel for A/B measurements:
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
@@ -52,6 +53,7 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
   }
   if (variant != 3 && nbricks < 2LL * nsm) return cudaSuccess;
   if (scheme == HJ_WENO5) return launch_brick_weno5(P, s, handled, variant);
+  if (scheme == HJ_WENO5_FMA) return launch_brick_weno5_fma(P, s, handled, variant);
   return launch_brick_eno(scheme, P, s, handled);
 }
 }  // namespace hj

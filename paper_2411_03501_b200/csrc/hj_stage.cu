@@ -76,6 +76,7 @@ cudaError_t launch_derivs(int scheme, const GridArgs& G, int axis, int eps_mode,
     case HJ_FIRST: k_derivs<HJ_FIRST><<<blocks, 256, 0, s>>>(G, axis, eps_mode, v, left, right); break;
     case HJ_ENO2: k_derivs<HJ_ENO2><<<blocks, 256, 0, s>>>(G, axis, eps_mode, v, left, right); break;
     case HJ_ENO3: k_derivs<HJ_ENO3><<<blocks, 256, 0, s>>>(G, axis, eps_mode, v, left, right); break;
+    case HJ_WENO5_FMA: k_derivs<HJ_WENO5_FMA><<<blocks, 256, 0, s>>>(G, axis, eps_mode, v, left, right); break;
     default: k_derivs<HJ_WENO5><<<blocks, 256, 0, s>>>(G, axis, eps_mode, v, left, right); break;
   }
   return cudaGetLastError();

@@ -82,6 +82,7 @@ static inline cudaError_t launch_stage_s(int scheme, const StageArgs& P, cudaStr
     case HJ_FIRST: return launch_stage_t<DIM, HJ_FIRST, HAM>(P, s);
     case HJ_ENO2: return launch_stage_t<DIM, HJ_ENO2, HAM>(P, s);
     case HJ_ENO3: return launch_stage_t<DIM, HJ_ENO3, HAM>(P, s);
+    case HJ_WENO5_FMA: return launch_stage_t<DIM, HJ_WENO5_FMA, HAM>(P, s);
     default: return launch_stage_t<DIM, HJ_WENO5, HAM>(P, s);
   }
 }

@@ -277,14 +277,14 @@ def solve_tube_slabs(g, target, cfg: TermConfig, horizon: float, global_steps: i
 
     from .integrator import IntegratorOptions
     from .reachability import BRTResult
-    from .spatial import GHOST_WIDTH
+    from .spatial import SCHEME_WIDTH
 
     rank, world = dist.get_rank(), dist.get_world_size()
     target_vals = np.asarray(target.values if hasattr(target, "values") else target, dtype=np.float64)
     if horizon == 0:
         return BRTResult(snapshots=(target,) if rank == 0 else (), times=(0.0,))
     opts = opts or IntegratorOptions()
-    halo = halo if halo is not None else max(GHOST_WIDTH[cfg.derivative_scheme], 2)
+    halo = halo if halo is not None else max(SCHEME_WIDTH[cfg.derivative_scheme], 2)
     si = SlabIntegrator(g, cfg, rank, world, halo=halo, transport=transport, group=group)
     slabs = partition(g.counts[0], world, halo, g.is_periodic(0))
     use_min = cfg.approximation_sign == "over"

@@ -15,6 +15,11 @@ from . import device as dev
 from .grid import Grid, ScalarField
 
 GHOST_WIDTH = {"first": 1, "eno2": 2, "eno3": 3, "weno5": 3}   # spatial.py:27
+# Schemes beyond the reference's registry: "weno5_fma" is WENO5 evaluated in
+# tolerance mode (FMA, reciprocal multiplies, one division per side; within
+# the north-star 1e-9 contract instead of bit-exact -- hjb200.h HJ_WENO5_FMA).
+TOLERANCE_SCHEMES = {"weno5_fma": 3}
+SCHEME_WIDTH = {**GHOST_WIDTH, **TOLERANCE_SCHEMES}
 
 
 @dataclass(frozen=True)
@@ -95,6 +100,12 @@ def upwind_first_weno5(g: Grid, f: ScalarField, axis: int, eps_mode: str = "squa
     return _pair(g, f, axis, "weno5", _eps_mode(eps_mode))
 
 
+def upwind_first_weno5_fma(g: Grid, f: ScalarField, axis: int) -> DerivativePair:
+    """WENO5 pair in tolerance mode (same scheme as upwind_first_weno5, "squared"
+    epsilon; agrees with it to rounding, not bitwise -- hjb200.h HJ_WENO5_FMA)."""
+    return _pair(g, f, axis, "weno5_fma")
+
+
 def weno5_workspace(g: Grid, f: ScalarField, axis: int, side: str = "left",
                     eps_mode: str = "squared") -> WenoWorkspace:
     """WENO smoothness / weight internals of one side (spatial.py:250-257)."""
@@ -126,6 +137,7 @@ _SCHEMES = {
     "eno2": upwind_first_eno2,
     "eno3": upwind_first_eno3,
     "weno5": upwind_first_weno5,
+    "weno5_fma": upwind_first_weno5_fma,
 }
 
 

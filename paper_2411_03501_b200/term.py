@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib
 from . import device as dev
 from .grid import Grid, ScalarField
-from .spatial import GHOST_WIDTH, DerivativePair
+from .spatial import SCHEME_WIDTH, DerivativePair
 
 Hamiltonian = Callable[[float, Grid, ScalarField, Sequence[ScalarField]], ScalarField]
 Partials = Callable[[float, Grid, ScalarField, Sequence[tuple[float, float]], int], float]
@@ -122,9 +122,9 @@ class TermConfig:
     approximation_sign: str = "over"
 
     def __post_init__(self) -> None:
-        if self.derivative_scheme not in GHOST_WIDTH:
+        if self.derivative_scheme not in SCHEME_WIDTH:
             raise ValueError(f"unknown derivative scheme {self.derivative_scheme!r}; "
-                             f"pick from {sorted(GHOST_WIDTH)}")
+                             f"pick from {sorted(SCHEME_WIDTH)}")
         if self.dissipation != "glf":
             raise ValueError(f"only 'glf' dissipation is available, got {self.dissipation!r}")
         if self.approximation_sign not in ("over", "under"):
