@@ -80,6 +80,12 @@ enum {
   HJ_STAGE_RK3_THIRD = 4     /* out = (y0 + 2.0*(y + dt*delta)) / 3.0                  */
 };
 
+/* parts of a stage launch along axis 0 (multi-GPU overlap):
+ * CORE = the owned planes whose stencils read no exchanged halo plane (runs
+ * while the halo exchange is in flight), RIM = the rest; CORE + RIM = ALL,
+ * bit for bit.  The split follows the kernel's own axis-0 tiling. */
+enum { HJ_PART_ALL = 0, HJ_PART_CORE = 1, HJ_PART_RIM = 2 };
+
 /* tube masks -- reachability.py:234,249 */
 enum { HJ_MASK_NONE = 0, HJ_MASK_MIN = 1, HJ_MASK_MAX = 2 };
 
@@ -182,6 +188,13 @@ int hj_weno5_workspace(const hj_grid* g, int axis, int side, int eps_mode,
 int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha,
              double dt, int stage, const double* y_in, const double* y0, double* y_out,
              const double* mask_prev, int mask, hj_stats* stats, int32_t tag, void* stream);
+
+/* hj_stage restricted to one axis-0 part (HJ_PART_*): on a slab with exchanged
+ * halos, launch CORE, wait for the exchange, launch RIM. */
+int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha,
+                  double dt, int stage, const double* y_in, const double* y0, double* y_out,
+                  const double* mask_prev, int mask, hj_stats* stats, int32_t tag, int part,
+                  void* stream);
 
 /* rockets_hamiltonian / rockets_hamiltonian_extremal / advection H as an API
  * call (reachability.py:61-116, term.py:136-140): out = H(x, p) with p an array

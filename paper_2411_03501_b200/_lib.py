@@ -29,6 +29,7 @@ CSG_UNION, CSG_INTERSECT, CSG_COMPLEMENT, CSG_DIFFERENCE = range(4)
 NF_INPUT, NF_DERIV, NF_HAM, NF_DELTA, NF_OUTPUT = 1, 2, 4, 8, 16
 FLAG_HAM_NONZERO = 32
 NF_MASK = 31
+PART_ALL, PART_CORE, PART_RIM = range(3)   # hj_stage_part (hjb200.h HJ_PART_*)
 
 
 class HjGrid(ctypes.Structure):
@@ -81,6 +82,8 @@ _SIGNATURES = [
     ("hj_weno5_workspace", c_int, [POINTER(HjGrid), c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("hj_stage", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_double, c_int,
                          c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_void_p]),
+    ("hj_stage_part", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_double, c_int,
+                              c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_int, c_void_p]),
     ("hj_term", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_void_p, c_void_p,
                         c_void_p, c_void_p]),
     ("hj_costates", c_int, [POINTER(HjGrid), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p),

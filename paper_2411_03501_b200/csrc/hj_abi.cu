@@ -220,15 +220,48 @@ int hj_weno5_workspace(const hj_grid* g, int axis, int side, int eps_mode, const
   return cuda_status(launch_weno_ws(G, axis, side, eps_mode, v, ws, (cudaStream_t)stream), "hj_weno5_workspace");
 }
 
-int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
-             const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
-             hj_stats* stats, int32_t tag, void* stream) {
+// Axis-0 rows of a stage launch.  part 0: every row; 1 (core): the rows whose
+// stencils read no exchanged halo plane (halo_lo / halo_hi), so they can run
+// while the exchange is in flight; 2 (rim): the rest.  unit = planes per row
+// (8 for the 3-D brick rows, 8 for the 4-D pre-pass segments, 1 for planes);
+// a row r covers planes [r*unit, r*unit+unit) and reads `reach` planes
+// further on each side.
+static RowSet row_set(int n0, int unit, int reach, int halo_lo, int halo_hi, int part) {
+  const int nrows = (n0 + unit - 1) / unit;
+  RowSet R{0, nrows, nrows, nrows};
+  if (part == HJ_PART_ALL) return R;
+  int lo = 0, hi = nrows;                                   // core rows [lo, hi)
+  if (halo_lo) lo = (reach + unit - 1) / unit;              // first row with r*unit >= reach
+  if (halo_hi) hi = (n0 - reach - unit) >= 0 ? (n0 - reach - unit) / unit + 1 : 0;   // r*unit+unit+reach <= n0
+  if (hi < lo) hi = lo;
+  if (part == HJ_PART_CORE) return RowSet{lo, hi - lo, hi, hi - lo};
+  return RowSet{0, lo, hi, lo + (nrows - hi)};              // HJ_PART_RIM
+}
+
+static void set_rows(StageArgs& P, int w, int part) {
+  const GridArgs& G = P.g;
+  const int hl = G.ax[0].halo_lo, hh = G.ax[0].halo_hi;
+  // the brick rows (3-D) and pre-pass segments (4-D) are both 8 planes deep;
+  // the per-node kernel and the 4-D brick slices work per plane
+  P.zr = row_set(G.n[0], 8, w, hl, hh, part);
+  const RowSet& r = P.zr;
+  // planes covered by those rows (clipped to the slab)
+  auto clip = [&](int row) { return row * 8 < G.n[0] ? row * 8 : G.n[0]; };
+  const int a0 = clip(r.lo), a1 = clip(r.lo + r.split), b0 = clip(r.hs), b1 = clip(r.hs + (r.cnt - r.split));
+  P.zp = RowSet{a0, a1 - a0, b0, (a1 - a0) + (b1 - b0)};
+}
+
+int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                  const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                  hj_stats* stats, int32_t tag, int part, void* stream) {
   const int w = ghost_width_of(scheme);
   if (w < 0) return fail(HJ_EINVAL, "unknown derivative scheme %d", scheme);
+  if (part < HJ_PART_ALL || part > HJ_PART_RIM) return fail(HJ_EINVAL, "unknown stage part %d", part);
   StageArgs P;
   std::memset(&P, 0, sizeof P);
   int rc = make_grid(g, w, &P.g);
   if (rc) return rc;
+  set_rows(P, w, part);
   rc = check_ham(ham, P.g.dim);
   if (rc) return rc;
   if (!alpha) return fail(HJ_EINVAL, "alpha is NULL");
@@ -272,6 +305,13 @@ int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alph
   return cuda_status(e, "hj_stage");
 }
 
+int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+             const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+             hj_stats* stats, int32_t tag, void* stream) {
+  return hj_stage_part(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag,
+                       HJ_PART_ALL, stream);
+}
+
 int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, const double* v,
             double* delta, hj_stats* stats, void* stream) {
   const int w = ghost_width_of(scheme);
@@ -280,6 +320,7 @@ int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha
   std::memset(&P, 0, sizeof P);
   int rc = make_grid(g, w, &P.g);
   if (rc) return rc;
+  set_rows(P, w, HJ_PART_ALL);
   rc = check_ham(ham, P.g.dim);
   if (rc) return rc;
   if (!alpha) return fail(HJ_EINVAL, "alpha is NULL");

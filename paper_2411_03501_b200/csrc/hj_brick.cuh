@@ -84,19 +84,23 @@ template <int AO>
 struct BrickView {
   int n0, n1, n2;
   long long s0, s1;
-  int slices;   // independent 3-D slices: batch (x n[0] when AO = 1)
-  __device__ __forceinline__ explicit BrickView(const GridArgs& G) {
+  int slices;   // independent 3-D slices: batch (x the launch's axis-0 planes when AO = 1)
+  RowSet zr, zp;
+  __device__ __forceinline__ explicit BrickView(const StageArgs& P) {
+    const GridArgs& G = P.g;
     n0 = G.n[AO];
     n1 = G.n[AO + 1];
     n2 = G.n[AO + 2];
     s0 = G.stride[AO];
     s1 = G.stride[AO + 1];
-    slices = AO ? G.batch * G.n[0] : G.batch;
+    zr = P.zr;
+    zp = P.zp;
+    slices = AO ? G.batch * zp.cnt : G.batch;
   }
   // element offset of slice b from problem 0's first owned node
   __device__ __forceinline__ long long slice_base(const GridArgs& G, int b) const {
     if (AO == 0) return (long long)b * G.batch_stride;
-    const int pb = b / G.n[0], i0 = b % G.n[0];
+    const int pb = b / zp.cnt, i0 = zp.map(b % zp.cnt);
     return (long long)pb * G.batch_stride + (long long)i0 * G.stride[0];
   }
 };
@@ -107,13 +111,15 @@ struct BrickCoord {
 
 template <int AO>
 __device__ __forceinline__ BrickCoord brick_coord(const BrickView<AO>& V, int lin) {
-  const int nbx = (V.n2 + BYX - 1) / BYX, nby = (V.n1 + BYX - 1) / BYX, nbz = (V.n0 + BZ - 1) / BZ;
+  // AO = 0: the launch's brick rows along the first axis (V.zr); AO = 1: every row
+  const int nbx = (V.n2 + BYX - 1) / BYX, nby = (V.n1 + BYX - 1) / BYX;
+  const int nbz = AO ? (V.n0 + BZ - 1) / BZ : V.zr.cnt;
   BrickCoord c;
   c.x0 = (lin % nbx) * BYX;
   lin /= nbx;
   c.y0 = (lin % nby) * BYX;
   lin /= nby;
-  c.z0 = (lin % nbz) * BZ;
+  c.z0 = (AO ? (lin % nbz) : V.zr.map(lin % nbz)) * BZ;
   c.b = lin / nbz;
   return c;
 }
@@ -152,7 +158,7 @@ template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P, int nbricks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(smem_raw);
-  const BrickView<AO> V(P.g);
+  const BrickView<AO> V(P);
   unsigned flags = 0u;
   // persistent CTAs: bricks blockIdx.x, +gridDim.x, ... (neighbouring CTAs take
   // neighbouring bricks, so halo rows are shared through L2)
@@ -384,8 +390,7 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   const long long plane = G.stride[0];
   const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= plane) return;
-  const int nseg = (G.n[0] + SEG - 1) / SEG;
-  const int seg = blockIdx.y % nseg, pb = blockIdx.y / nseg;
+  const int seg = P.zr.map(blockIdx.y % P.zr.cnt), pb = blockIdx.y / P.zr.cnt;
   const int z0 = seg * SEG;
   const long long base = (long long)pb * G.batch_stride + pos;
   const double* col = P.y_in + base;
@@ -416,16 +421,17 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
     if (dev >= 0 && dev < 64) configured[dev] = true;
   }
   const GridArgs& G = P.g;
-  const long long slices = AO ? (long long)G.batch * G.n[0] : G.batch;
+  const long long slices = AO ? (long long)G.batch * P.zp.cnt : G.batch;
   const long long nbricks = (long long)((G.n[AO + 2] + BYX - 1) / BYX) * ((G.n[AO + 1] + BYX - 1) / BYX) *
-                            ((G.n[AO] + BZ - 1) / BZ) * slices;
+                            (AO ? (G.n[AO] + BZ - 1) / BZ : P.zr.cnt) * slices;
+  if (nbricks == 0) return cudaSuccess;
   static int sms[64] = {};
   if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
   if (AO) {
     const long long plane = G.stride[0];
-    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(((G.n[0] + SEG - 1) / SEG) * G.batch));
+    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(P.zr.cnt * G.batch));
     k_axis0_walk<SCHEME><<<pg, 256, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

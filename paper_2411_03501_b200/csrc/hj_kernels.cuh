@@ -18,8 +18,20 @@ struct GridArgs {
   const double* nodes[HJ_MAX_DIM];
 };
 
+// A subset of axis-0 rows (bricks rows, pre-pass segments or single planes):
+// rows lo .. lo+split-1, then hs .. hs+(cnt-split)-1 (hj_stage_part splits).
+struct RowSet {
+  int lo, split, hs, cnt;
+  __host__ __device__ __forceinline__ int map(int k) const { return k < split ? lo + k : hs + (k - split); }
+  __host__ __device__ __forceinline__ bool has(int r) const {
+    return (r >= lo && r < lo + split) || (r >= hs && r < hs + (cnt - split));
+  }
+};
+
 struct StageArgs {
   GridArgs g;
+  RowSet zr;        // axis-0 brick rows (3-D brick) / pre-pass segments (4-D) of this launch
+  RowSet zp;        // axis-0 planes of this launch (per-node kernel, 4-D brick slices)
   hj_ham ham;
   double alpha_half[HJ_MAX_DIM];  // alphas[i] * 0.5 (term.py:86)
   double dt;

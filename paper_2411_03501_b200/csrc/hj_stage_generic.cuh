@@ -21,9 +21,9 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
 #pragma unroll
   for (int a = 0; a < DIM; ++a) { lo[a] = KEY_POS_INF; hi[a] = KEY_NEG_INF; }
 
-  if (idx < total) {
-    int ix[HJ_MAX_DIM];
-    const long long off = locate(P.g, idx, ix);
+  int ix[HJ_MAX_DIM];
+  const long long off = idx < total ? locate(P.g, idx, ix) : 0;
+  if (idx < total && P.zp.has(ix[0])) {
     double pbar[DIM];
     double diss = 0.0;
 #pragma unroll

@@ -86,12 +86,16 @@ class TorchDistTransport:
         self.slab = slab
         self.group = group
 
-    def exchange(self, buf: torch.Tensor) -> None:
+    def start(self, buf: torch.Tensor):
+        """Post the halo exchange of ``buf``; returns what ``finish`` waits on.
+        NCCL: the sends/receives run on NCCL's stream, ordered after the work
+        already queued on the current stream, so the caller can launch the
+        CORE part of the stage (which reads no halo plane) meanwhile."""
         import torch.distributed as dist
 
         sends, recvs = halo_plan(self.slab)
         if not sends and not recvs:
-            return
+            return None
         staged = buf.is_cuda and dist.get_backend(self.group) != "nccl"
         if staged:
             # gloo moves host tensors only: stage the halo planes through the host
@@ -103,11 +107,22 @@ class TorchDistTransport:
             rbufs = [buf[a:b] for _, (a, b) in recvs]
         ops = [dist.P2POp(dist.isend, t, peer, self.group) for (peer, _), t in zip(sends, sbufs)]
         ops += [dist.P2POp(dist.irecv, t, peer, self.group) for (peer, _), t in zip(recvs, rbufs)]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+        works = dist.batch_isend_irecv(ops)
         if staged:
+            for w in works:
+                w.wait()
             for (_, (a, b)), t in zip(recvs, rbufs):
                 buf[a:b].copy_(t)
+            return None
+        return works
+
+    def finish(self, pending) -> None:
+        """Order the current stream after the exchange (NCCL: no host wait)."""
+        for w in pending or ():
+            w.wait()
+
+    def exchange(self, buf: torch.Tensor) -> None:
+        self.finish(self.start(buf))
 
     def max_flags(self, flags: int) -> int:
         import torch.distributed as dist
@@ -126,8 +141,11 @@ class SlabIntegrator(FusedIntegrator):
     return full buffers.
     """
 
-    def __init__(self, g, cfg: TermConfig, rank: int, world: int, halo: int = 3, transport=None, group=None):
+    def __init__(self, g, cfg: TermConfig, rank: int, world: int, halo: int = 3, transport=None, group=None,
+                 overlap: bool = True):
         self.slab = partition(g.counts[0], world, halo, g.is_periodic(0))[rank]
+        # overlap: each stage = CORE launch while the halo exchange is in flight, then RIM
+        self.overlap = overlap
         s = self.slab
         dg = dev.DeviceGrid(g, slab=(s.lo, s.n, int(s.has_lo), int(s.has_hi), s.halo))
         self.transport = transport or TorchDistTransport(s, group)
@@ -163,11 +181,19 @@ class SlabIntegrator(FusedIntegrator):
         return self._bufs
 
     def _stage(self, alphas_c, dt, kind, y_in, y0, y_out, mask_prev, mask, tag, strm):
-        self.transport.exchange(y_in)
         o = self.owned
-        dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, o(y_in), None if y0 is None else o(y0),
-                      o(y_out), None if mask_prev is None else o(mask_prev), mask, self.stats, tag, lib=self.lib,
-                      strm=strm)
+        args = (self.dg, self.scheme, self.dh, alphas_c, dt, kind, o(y_in), None if y0 is None else o(y0),
+                o(y_out), None if mask_prev is None else o(mask_prev), mask, self.stats, tag)
+        if self.overlap and (self.slab.has_lo or self.slab.has_hi):
+            # halo exchange in flight while the core planes compute; the rim after it
+            pending = self.transport.start(y_in)
+            dev.stage_dev(*args, lib=self.lib, strm=strm, part=_lib.PART_CORE)
+            self.transport.finish(pending)
+            dev.stage_dev(*args, lib=self.lib, strm=strm, part=_lib.PART_RIM)
+            self.launches += 2
+            return
+        self.transport.exchange(y_in)
+        dev.stage_dev(*args, lib=self.lib, strm=strm)
         self.launches += 1
 
     def _raise_pending(self, times, warn: bool = False) -> None:
@@ -200,6 +226,12 @@ class LocalTransport:
 class _LocalEndpoint:
     def __init__(self, hub: LocalTransport, rank: int):
         self.hub, self.rank = hub, rank
+
+    def start(self, buf: torch.Tensor):
+        self.exchange(buf)
+
+    def finish(self, pending) -> None:
+        pass
 
     def exchange(self, buf: torch.Tensor) -> None:
         s = self.hub.slabs[self.rank]
