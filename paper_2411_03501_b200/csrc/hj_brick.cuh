@@ -193,18 +193,48 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
 
   const bool zin = (z0 >= HB || A0.halo_lo) && (z0 + BZ + HB <= n0 || A0.halo_hi);
   const bool interior = zin && z0 + BZ <= n0 && y0 >= HB && y0 + BYX + HB <= n1 && x0 >= HB && x0 + BYX + HB <= n2;
-  if (interior) {
-    // ---- load, interior brick: every value is in memory.  cp.async (8 B per
-    // element) puts all of the brick's loads in flight at once without
-    // staging them in registers; the plane corners (never read) are skipped.
+  // ---- load.  Warp w owns brick plane z = w: it walks the plane's 22 rows
+  // (second-axis halo rows included) with one incrementing row pointer, lane
+  // = third-axis position (halo columns included); plane corners are never
+  // read and skipped.  In-domain values go global -> shared with cp.async
+  // (8 B, no register staging, all in flight at once); ghosts (boundary
+  // bricks only) are synthesised by fetch() and stored directly.
+  {
+    static_assert(BZ == BRICK_THREADS / 32, "one warp per brick plane");
     const int lane = t & 31, warp = t >> 5;
-    const double* vbase = vin + (z0 * s0 + (y0 - HB) * s1 + (x0 - HB));
+    const int z = warp, gz = z0 + z;
+    const int gx = x0 - HB + lane;
     const bool xin = lane >= HB && lane < HB + BYX;
+    const bool lane_on = lane < SVR;
+    const bool gx_in = gx >= 0 && gx < n2;
+    double* srow = &S.v[z * PLANE + lane];
+    if (interior) {
+      const double* grow = vin + (gz * s0 + (y0 - HB) * s1 + gx);
 #pragma unroll 2
-    for (int row = warp; row < BZ * SVR; row += BRICK_THREADS / 32) {   // 22 rows per warp
-      const int z = row / SVR, yy = row % SVR;
-      const bool yin = yy >= HB && yy < HB + BYX;
-      if (lane < SVR && (yin || xin)) cp_async8(&S.v[z * PLANE + yy * SVP + lane], vbase + z * s0 + yy * s1 + lane);
+      for (int yy = 0; yy < SVR; ++yy, grow += s1, srow += SVP) {
+        const bool yin = yy >= HB && yy < HB + BYX;
+        if (lane_on && (yin || xin)) cp_async8(srow, grow);
+      }
+    } else {
+      for (int yy = 0; yy < SVR; ++yy, srow += SVP) {
+        const bool yin = yy >= HB && yy < HB + BYX;
+        if (!lane_on || !(yin || xin)) continue;
+        const int gy = y0 + yy - HB;
+        const bool gy_in = gy >= 0 && gy < n1;
+        if (gz < n0) {
+          if (gy_in && gx_in) {
+            cp_async8(srow, vin + (gz * s0 + gy * s1 + gx));
+          } else {
+            double val = 0.0;
+            if (gx_in) val = fetch(vin + gz * s0 + gx, A1, gy);          // second-axis ghost
+            else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, A2, gx);  // third-axis ghost
+            *srow = val;
+          }
+        } else {
+          // beyond the last plane of a partial brick: first-axis ghosts (read by the first-axis walk)
+          *srow = (gy_in && gx_in) ? fetch(vin + gy * s1 + gx, A0, gz) : 0.0;
+        }
+      }
     }
     // first-axis halo planes: 6 x 16 rows of 16, two rows per warp instruction
     const int half = lane >> 4, xl = lane & (BYX - 1);
@@ -213,38 +243,15 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       const int row = 2 * r2 + half;
       const int k = row / BYX, y = row % BYX;
       const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
-      cp_async8(&S.zh[row * BYX + xl], vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
+      double* dst = &S.zh[row * BYX + xl];
+      if (interior) {
+        cp_async8(dst, vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
+      } else {
+        const int gy = y0 + y, gxx = x0 + xl;
+        *dst = (gy < n1 && gxx < n2) ? fetch(vin + gy * s1 + gxx, A0, e) : 0.0;
+      }
     }
     cp_async_wait_all();
-  } else {
-    // ---- load, boundary brick: planes with second/third-axis halos (corners unused)
-    for (int q = t; q < BZ * SVR * SVR; q += BRICK_THREADS) {
-      const int z = q / (SVR * SVR), r = q % (SVR * SVR);
-      const int yy = r / SVR, xx = r % SVR;
-      const bool yin = yy >= HB && yy < HB + BYX, xin = xx >= HB && xx < HB + BYX;
-      if (!yin && !xin) continue;
-      const int gz = z0 + z, gy = y0 + yy - HB, gx = x0 + xx - HB;
-      double val = 0.0;
-      const bool gy_in = gy >= 0 && gy < n1, gx_in = gx >= 0 && gx < n2;
-      if (gz < n0) {
-        if (gy_in && gx_in) val = vin[gz * s0 + gy * s1 + gx];
-        else if (gx_in) val = fetch(vin + gz * s0 + gx, A1, gy);          // second-axis ghost
-        else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, A2, gx);     // third-axis ghost
-      } else if (gy_in && gx_in) {
-        val = fetch(vin + gy * s1 + gx, A0, gz);                           // first-axis ghost (partial brick)
-      }
-      S.v[z * PLANE + yy * SVP + xx] = val;
-    }
-    // first-axis halo planes (exchanged planes or boundary ghosts)
-    for (int q = t; q < 2 * HB * BYX * BYX; q += BRICK_THREADS) {
-      const int k = q / (BYX * BYX), yx = q % (BYX * BYX);
-      const int y = yx / BYX, x = yx % BYX;
-      const int gy = y0 + y, gx = x0 + x;
-      const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
-      double val = 0.0;
-      if (gy < n1 && gx < n2) val = fetch(vin + gy * s1 + gx, A0, e);
-      S.zh[q] = val;
-    }
   }
   // the Hamiltonian's node-table inputs for this brick (global loads once per
   // brick instead of per node)
