@@ -273,6 +273,21 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   __syncthreads();
   if (next) prefetch_brick<AO>(G, V, P.y_in, *next, t);
 
+  // the first-axis walk's y0 inputs (RK2/RK3 combination stages) are read two
+  // nodes ahead; the first two are issued here so that their latency hides
+  // behind the second/third-axis walks
+  constexpr int QD = 2;
+  const int cy = t / BYX, cx = t % BYX;
+  const bool col_on = y0 + cy < n1 && x0 + cx < n2;
+  const long long coff0 = (long long)z0 * s0 + (long long)(y0 + cy) * s1 + (x0 + cx);
+  const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
+  const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
+  const int zmax = n0 - z0;   // nodes of this column inside the domain (may exceed BZ)
+  double qy[QD];
+#pragma unroll
+  for (int k = 0; k < QD; ++k)
+    qy[k] = (col_on && need_y0 && k < zmax && k < BZ) ? y0p[coff0 + (long long)k * s0] : 0.0;
+
   // ---- second and third brick axes together: warps 0-3 walk the BZ x BYX
   // lines along y, warps 4-7 the lines along x, each a whole 16-node edge;
   // they leave p_avg and the dissipation term of their axis per node
@@ -309,25 +324,21 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   //   (integrator.py:93-103), the optional tube mask (reachability.py:249),
   // the non-finite flags, and stores the node (coalesced across x).
   {
-    const int y = t / BYX, x = t % BYX;
-    if (y0 + y < n1 && x0 + x < n2) {
+    const int y = cy, x = cx;
+    if (col_on) {
       const double* col = &S.v[(y + HB) * SVP + (x + HB)];
       const double* zlo = &S.zh[HB * BYX * BYX + y * BYX + x];          // plane k+3, k in [-3,-1]
       const double* zhi = &S.zh[(HB - BZ) * BYX * BYX + y * BYX + x];   // plane k-BZ+3, k >= BZ
       const double ah = P.alpha_half[AO];
       const int s00 = swz(0, y, x);
-      const int zmax = n0 - z0;   // nodes of this column inside the domain (may exceed BZ)
-      const long long off0 = (long long)z0 * s0 + (long long)(y0 + y) * s1 + (x0 + x);
-      const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
+      const long long off0 = coff0;
       const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
       double* __restrict__ out = P.y_out + base;
-      const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
       const bool need_m = P.mask != HJ_MASK_NONE;
-      // global inputs of the node being emitted, fetched one node ahead
-      double nz_y0 = 0.0, nz_m = 0.0, nz_p0 = 0.0, nz_d0 = 0.0;
+      // other global inputs of the node being emitted, fetched one node ahead
+      double nz_m = 0.0, nz_p0 = 0.0, nz_d0 = 0.0;
       auto fetch_node = [&](int i) {
         const long long off = off0 + (long long)i * s0;
-        nz_y0 = need_y0 ? y0p[off] : 0.0;
         nz_m = need_m ? mp[off] : 0.0;
         if (AO) {
           nz_p0 = P.aux_p0[base + off];
@@ -342,7 +353,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       };
       auto emit = [&](int i, double L, double R) {
         if (i >= zmax) return;
-        const double yz = nz_y0, pv = nz_m, a0 = nz_p0, d0 = nz_d0;
+        const double yz = qy[0], pv = nz_m, a0 = nz_p0, d0 = nz_d0;
+#pragma unroll
+        for (int k = 0; k + 1 < QD; ++k) qy[k] = qy[k + 1];
+        qy[QD - 1] = (need_y0 && i + QD < zmax && i + QD < BZ) ? y0p[off0 + (long long)(i + QD) * s0] : 0.0;
         if (i + 1 < zmax && i + 1 < BZ) fetch_node(i + 1);
         const int s = s00 + i * (BYX * BYX);
         double p[3 + AO];

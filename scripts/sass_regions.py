@@ -29,3 +29,19 @@ allS = sum(samp.values())
 for k in sorted(tot):
     print(f"region {k}: samples {samp[k]/allS*100:5.1f}%  instr {tot[k]:>12d}  top: " +
           ", ".join(f"{c}:{v}" for c, v in mix[k].most_common(8)))
+
+# stall reasons per region
+cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+idx = [hdr.index(c) for c in cols]
+region = 0
+st = defaultdict(Counter)
+for r in data:
+    src = r[iS].strip()
+    for c, i in zip(cols, idx):
+        st[region][c] += int(r[i] or 0)
+    base = re.sub(r"^@!?U?P\w+\s+", "", src).split(" ")[0].split(".")[0]
+    if base == "BAR":
+        region += 1
+for k in sorted(st):
+    tot_k = sum(st[k].values()) or 1
+    print(f"region {k} stalls: " + ", ".join(f"{c[6:]}:{v/allS*100:.1f}" for c, v in st[k].most_common(6)))
