@@ -196,9 +196,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // ---- load.  Warp w owns brick plane z = w: it walks the plane's 22 rows
   // (second-axis halo rows included) with one incrementing row pointer, lane
   // = third-axis position (halo columns included); plane corners are never
-  // read and skipped.  In-domain values go global -> shared with cp.async
-  // (8 B, no register staging, all in flight at once); ghosts (boundary
-  // bricks only) are synthesised by fetch() and stored directly.
+  // read and skipped.  Values in memory go global -> shared with cp.async
+  // (8 B, no register staging, all in flight at once); on boundary bricks the
+  // extrapolated / dirichlet ghosts are then synthesised from the landed edge
+  // nodes (no synchronous global loads on the load path).
   {
     static_assert(BZ == BRICK_THREADS / 32, "one warp per brick plane");
     const int lane = t & 31, warp = t >> 5;
@@ -216,39 +217,99 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         if (lane_on && (yin || xin)) cp_async8(srow, grow);
       }
     } else {
+      // boundary brick, phase 1: every value that lives in memory (in-domain,
+      // periodic wrap, exchanged halo planes) goes through cp.async; the
+      // extrapolated / dirichlet ghosts wait for their edge nodes (phase 2)
+      const int jx = ghost_index(A2, gx);
+      const int jz = ghost_index(A0, gz);
       for (int yy = 0; yy < SVR; ++yy, srow += SVP) {
         const bool yin = yy >= HB && yy < HB + BYX;
         if (!lane_on || !(yin || xin)) continue;
         const int gy = y0 + yy - HB;
         const bool gy_in = gy >= 0 && gy < n1;
         if (gz < n0) {
-          if (gy_in && gx_in) {
-            cp_async8(srow, vin + (gz * s0 + gy * s1 + gx));
+          if (!gy_in && !gx_in) {
+            *srow = 0.0;   // outside the domain on both walk axes: never read
           } else {
-            double val = 0.0;
-            if (gx_in) val = fetch(vin + gz * s0 + gx, A1, gy);          // second-axis ghost
-            else if (gy_in) val = fetch(vin + gz * s0 + gy * s1, A2, gx);  // third-axis ghost
-            *srow = val;
+            const int jy = gy_in ? gy : ghost_index(A1, gy);
+            const int jxx = gx_in ? gx : jx;
+            if (jy != GI_SYNTH && jxx != GI_SYNTH) cp_async8(srow, vin + (gz * s0 + jy * s1 + jxx));
           }
-        } else {
+        } else if (gy_in && gx_in) {
           // beyond the last plane of a partial brick: first-axis ghosts (read by the first-axis walk)
-          *srow = (gy_in && gx_in) ? fetch(vin + gy * s1 + gx, A0, gz) : 0.0;
+          if (jz == GI_ZERO) *srow = 0.0;
+          else if (jz != GI_SYNTH) cp_async8(srow, vin + ((long long)jz * s0 + gy * s1 + gx));
+        } else {
+          *srow = 0.0;   // never read
         }
       }
-    }
-    // first-axis halo planes: 6 x 16 rows of 16, two rows per warp instruction
-    const int half = lane >> 4, xl = lane & (BYX - 1);
+      // first-axis halo planes (interior rows and columns of the brick only)
+      const int half = lane >> 4, xl = lane & (BYX - 1);
 #pragma unroll
-    for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
-      const int row = 2 * r2 + half;
-      const int k = row / BYX, y = row % BYX;
-      const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
-      double* dst = &S.zh[row * BYX + xl];
-      if (interior) {
-        cp_async8(dst, vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
-      } else {
+      for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
+        const int row = 2 * r2 + half;
+        const int k = row / BYX, y = row % BYX;
+        const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+        const int je = ghost_index(A0, e);
         const int gy = y0 + y, gxx = x0 + xl;
-        *dst = (gy < n1 && gxx < n2) ? fetch(vin + gy * s1 + gxx, A0, e) : 0.0;
+        double* dst = &S.zh[row * BYX + xl];
+        if (gy >= n1 || gxx >= n2 || je == GI_ZERO) *dst = 0.0;
+        else if (je != GI_SYNTH) cp_async8(dst, vin + ((long long)je * s0 + gy * s1 + gxx));
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // phase 2: synthesise the remaining ghosts from the landed edge nodes
+      // plane value at relative first-axis index r (-HB..BZ+HB-1) for an
+      // interior (y, x) of the brick, from S.v or the zh planes
+      auto pz = [&](int r, int y, int x) -> double {
+        if (r < 0) return S.zh[((r + HB) * BYX + y) * BYX + x];
+        if (r >= BZ) return S.zh[((r - BZ + HB) * BYX + y) * BYX + x];
+        return S.v[r * PLANE + (y + HB) * SVP + (x + HB)];
+      };
+      srow = &S.v[z * PLANE + lane];
+      for (int yy = 0; yy < SVR; ++yy, srow += SVP) {
+        const bool yin = yy >= HB && yy < HB + BYX;
+        if (!lane_on || !(yin || xin)) continue;
+        const int gy = y0 + yy - HB;
+        const bool gy_in = gy >= 0 && gy < n1;
+        if (gz < n0) {
+          if (!gy_in && !gx_in) continue;
+          if (!gy_in && ghost_index(A1, gy) == GI_SYNTH) {          // second-axis ghost
+            const int ye = (gy < 0 ? 0 : n1 - 1) - y0 + HB, yi = (gy < 0 ? 1 : n1 - 2) - y0 + HB;
+            *srow = ghost_synth(A1, gy, S.v[z * PLANE + ye * SVP + lane], S.v[z * PLANE + yi * SVP + lane]);
+          } else if (!gx_in && jx == GI_SYNTH) {                     // third-axis ghost
+            const int xe = (gx < 0 ? 0 : n2 - 1) - x0 + HB, xi = (gx < 0 ? 1 : n2 - 2) - x0 + HB;
+            *srow = ghost_synth(A2, gx, S.v[z * PLANE + yy * SVP + xe], S.v[z * PLANE + yy * SVP + xi]);
+          }
+        } else if (gy_in && gx_in && jz == GI_SYNTH) {                 // first-axis ghost
+          const int re = n0 - 1 - z0, ri = n0 - 2 - z0;   // re in [0, BZ), ri >= -1
+          const double edge = S.v[re * PLANE + yy * SVP + lane];
+          double inner;
+          if (ri >= 0) inner = S.v[ri * PLANE + yy * SVP + lane];
+          else if (yin && xin) inner = pz(ri, yy - HB, lane - HB);
+          else inner = vin[(long long)(n0 - 2) * s0 + gy * s1 + gx];
+          *srow = ghost_synth(A0, gz, edge, inner);
+        }
+      }
+#pragma unroll
+      for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
+        const int row = 2 * r2 + half;
+        const int k = row / BYX, y = row % BYX;
+        const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+        if (y0 + y >= n1 || x0 + xl >= n2 || ghost_index(A0, e) != GI_SYNTH) continue;
+        const int re = (e < 0 ? 0 : n0 - 1) - z0, ri = (e < 0 ? 1 : n0 - 2) - z0;
+        S.zh[row * BYX + xl] = ghost_synth(A0, e, pz(re, y, xl), pz(ri, y, xl));
+      }
+    }
+    // first-axis halo planes of an interior brick: 6 x 16 rows of 16, two rows per warp instruction
+    if (interior) {
+      const int half = lane >> 4, xl = lane & (BYX - 1);
+#pragma unroll
+      for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
+        const int row = 2 * r2 + half;
+        const int k = row / BYX, y = row % BYX;
+        const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+        cp_async8(&S.zh[row * BYX + xl], vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
       }
     }
     cp_async_wait_all();
@@ -276,7 +337,9 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // the first-axis walk's y0 inputs (RK2/RK3 combination stages) are read two
   // nodes ahead; the first two are issued here so that their latency hides
   // behind the second/third-axis walks
-  constexpr int QD = 2;
+  // (3-D only: the 4-D kernel has no registers to spare across the walks, it
+  // reads them one node ahead inside the first-axis walk)
+  constexpr int QD = AO ? 1 : 2;
   const int cy = t / BYX, cx = t % BYX;
   const bool col_on = y0 + cy < n1 && x0 + cx < n2;
   const long long coff0 = (long long)z0 * s0 + (long long)(y0 + cy) * s1 + (x0 + cx);
@@ -284,9 +347,11 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
   const int zmax = n0 - z0;   // nodes of this column inside the domain (may exceed BZ)
   double qy[QD];
+  if constexpr (AO == 0) {
 #pragma unroll
-  for (int k = 0; k < QD; ++k)
-    qy[k] = (col_on && need_y0 && k < zmax && k < BZ) ? y0p[coff0 + (long long)k * s0] : 0.0;
+    for (int k = 0; k < QD; ++k)
+      qy[k] = (col_on && need_y0 && k < zmax && k < BZ) ? y0p[coff0 + (long long)k * s0] : 0.0;
+  }
 
   // ---- second and third brick axes together: warps 0-3 walk the BZ x BYX
   // lines along y, warps 4-7 the lines along x, each a whole 16-node edge;
@@ -332,6 +397,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       const double ah = P.alpha_half[AO];
       const int s00 = swz(0, y, x);
       const long long off0 = coff0;
+      const int slice0 = AO ? V.zp.map(c.b % V.zp.cnt) : 0;   // 4-D: the slice's axis-0 index
       const double* __restrict__ mp = P.mask_prev ? P.mask_prev + base : nullptr;
       double* __restrict__ out = P.y_out + base;
       const bool need_m = P.mask != HJ_MASK_NONE;
@@ -346,6 +412,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         }
       };
       fetch_node(0);
+      if constexpr (AO != 0) qy[0] = need_y0 ? y0p[coff0] : 0.0;
       auto ld = [&](int k) -> double {
         if (k < 0) return zlo[k * (BYX * BYX)];
         if (k < BZ) return col[k * PLANE];
@@ -382,7 +449,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
           cin[2] = S.crd[CRD_T0 + x];
           cin[3] = S.crd[CRD_T1 + x];
         } else {
-          int ix[4] = {c.b % G.n[0], z0 + i, y0 + y, x0 + x};
+          int ix[4] = {slice0, z0 + i, y0 + y, x0 + x};
           ham_inputs<HAM, 4>(P.ham, G.nodes, ix, cin);
         }
         const double H = ham_eval<HAM, 3 + AO>(P.ham, cin, p);

@@ -90,21 +90,22 @@ def steps_rate(g, cfg, y, k=5, w=2, dg=None):
     return s.elapsed_time(e) / 1e3 / k
 
 
-def c4():
+def c4(scheme="weno5"):
     n = int(os.environ.get("C4_N", "121"))
     g = hj.di4_grid(n)
-    cfg = hj.di4_term_config(scheme="weno5")
+    cfg = hj.di4_term_config(scheme=scheme)
     dg = dev.device_grid(g)
     y = dev.init_shape_dev(dg, _lib.SHAPE_CYLINDER, [0.0, 0.0, 0.0, 0.0, 2.0, 12.0])
     sec = steps_rate(g, cfg, y, k=3, w=1)
     cells = n ** 4
-    return {"config": f"C4 double-integrator pair {n}^4 WENO5+LF+RK3, 1 GPU", "ms_per_rk3_step": sec * 1e3,
+    return {"config": f"C4 double-integrator pair {n}^4 WENO5+LF+RK3, 1 GPU", "scheme": scheme,
+            "ms_per_rk3_step": sec * 1e3,
             "cell_updates_per_s": cells * 3 / sec}
 
 
-def c5():
+def c5(scheme="weno5"):
     g = hj.air3d_grid(101)
-    cfg = hj.air3d_term_config(scheme="weno5")
+    cfg = hj.air3d_term_config(scheme=scheme)
     B = 8
     rng = np.random.default_rng(0)
     targets = []
@@ -115,13 +116,13 @@ def c5():
     y = dev.to_dev(np.stack(targets))
     sec = steps_rate(g, cfg, y, k=5, w=2, dg=dg)
     cells = B * 101 ** 3
-    return {"config": "C5 batch of 8 Air3D 101^3 WENO5+LF+RK3 problems (one GPU's share of 64)",
+    return {"config": "C5 batch of 8 Air3D 101^3 WENO5+LF+RK3 problems (one GPU's share of 64)", "scheme": scheme,
             "ms_per_rk3_step": sec * 1e3, "cell_updates_per_s": cells * 3 / sec}
 
 
-def c2s():
+def c2s(scheme="weno5"):
     g = hj.air3d_grid(301)
-    cfg = hj.air3d_term_config(scheme="weno5")
+    cfg = hj.air3d_term_config(scheme=scheme)
     target = hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0)
     horizon = 0.02
     hj.solve_tube(g, target, cfg, 0.002, 1)
@@ -130,11 +131,14 @@ def c2s():
     dt = 0.5 / float(np.sum(alphas / g.spacings))
     steps = sum(int(np.ceil((horizon / 4) / dt - 1e-12)) for _ in range(4))
     return {"config": "C2 Air3D 301^3 WENO5 solve_tube, horizon 0.02 in 4 intervals (public API, snapshots to host, median of 3)",
+            "scheme": scheme,
             "seconds": secs, "approx_rk3_steps": steps,
             "cell_updates_per_s": 301 ** 3 * 3 * steps / secs}
 
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c1", "c5", "c4", "c2s"]
-    for name in which:
-        print(json.dumps({name: globals()[name]()}), flush=True)
+    for spec in which:   # name or name:scheme (e.g. c4:weno5_fma)
+        name, _, scheme = spec.partition(":")
+        out = globals()[name](scheme) if scheme else globals()[name]()
+        print(json.dumps({spec: out}), flush=True)
