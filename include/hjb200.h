@@ -196,6 +196,17 @@ int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double*
                   const double* mask_prev, int mask, hj_stats* stats, int32_t tag, int part,
                   void* stream);
 
+/* hj_stage over the owned axis-0 planes [plane_lo, plane_hi) only (a pipeline
+ * stage consuming host->device chunks as they land / producing device->host
+ * chunks as they finish): plane_lo a multiple of HJ_ROW_PLANES, plane_hi a
+ * multiple of it or n[0].  Reads planes plane_lo-w .. plane_hi+w-1 of y_in
+ * (w = the scheme's ghost width), writes only [plane_lo, plane_hi). */
+#define HJ_ROW_PLANES 8
+int hj_stage_planes(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha,
+                    double dt, int stage, const double* y_in, const double* y0, double* y_out,
+                    const double* mask_prev, int mask, hj_stats* stats, int32_t tag,
+                    int64_t plane_lo, int64_t plane_hi, void* stream);
+
 /* rockets_hamiltonian / rockets_hamiltonian_extremal / advection H as an API
  * call (reachability.py:61-116, term.py:136-140): out = H(x, p) with p an array
  * of dim device pointers to costate fields. */

@@ -84,6 +84,9 @@ _SIGNATURES = [
                          c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_void_p]),
     ("hj_stage_part", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_double, c_int,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_int, c_void_p]),
+    ("hj_stage_planes", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_double, c_int,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_int64, c_int64,
+                                c_void_p]),
     ("hj_term", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_void_p, c_void_p,
                         c_void_p, c_void_p]),
     ("hj_costates", c_int, [POINTER(HjGrid), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p),

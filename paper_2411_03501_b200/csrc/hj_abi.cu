@@ -226,6 +226,8 @@ int hj_weno5_workspace(const hj_grid* g, int axis, int side, int eps_mode, const
 // (8 for the 3-D brick rows, 8 for the 4-D pre-pass segments, 1 for planes);
 // a row r covers planes [r*unit, r*unit+unit) and reads `reach` planes
 // further on each side.
+constexpr int STAGE_PLANES = 3;   // internal: an explicit plane range (hj_stage_planes)
+
 static RowSet row_set(int n0, int unit, int reach, int halo_lo, int halo_hi, int part) {
   const int nrows = (n0 + unit - 1) / unit;
   RowSet R{0, nrows, nrows, nrows};
@@ -238,8 +240,14 @@ static RowSet row_set(int n0, int unit, int reach, int halo_lo, int halo_hi, int
   return RowSet{0, lo, hi, lo + (nrows - hi)};              // HJ_PART_RIM
 }
 
-static void set_rows(StageArgs& P, int w, int part) {
+static void set_rows(StageArgs& P, int w, int part, int64_t plo = 0, int64_t phi = 0) {
   const GridArgs& G = P.g;
+  if (part == STAGE_PLANES) {   // explicit plane range [plo, phi), validated by the caller
+    const int r0 = (int)(plo / 8), r1 = (int)((phi + 7) / 8);
+    P.zr = RowSet{r0, r1 - r0, r1, r1 - r0};
+    P.zp = RowSet{(int)plo, (int)(phi - plo), (int)phi, (int)(phi - plo)};
+    return;
+  }
   const int hl = G.ax[0].halo_lo, hh = G.ax[0].halo_hi;
   // the brick rows (3-D) and pre-pass segments (4-D) are both 8 planes deep;
   // the per-node kernel and the 4-D brick slices work per plane
@@ -251,17 +259,23 @@ static void set_rows(StageArgs& P, int w, int part) {
   P.zp = RowSet{a0, a1 - a0, b0, (a1 - a0) + (b1 - b0)};
 }
 
-int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
-                  const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
-                  hj_stats* stats, int32_t tag, int part, void* stream) {
+static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                      const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                      hj_stats* stats, int32_t tag, int part, int64_t plo, int64_t phi, void* stream) {
   const int w = ghost_width_of(scheme);
   if (w < 0) return fail(HJ_EINVAL, "unknown derivative scheme %d", scheme);
-  if (part < HJ_PART_ALL || part > HJ_PART_RIM) return fail(HJ_EINVAL, "unknown stage part %d", part);
   StageArgs P;
   std::memset(&P, 0, sizeof P);
   int rc = make_grid(g, w, &P.g);
   if (rc) return rc;
-  set_rows(P, w, part);
+  if (part == STAGE_PLANES) {
+    const int64_t n0 = P.g.n[0];
+    if (plo < 0 || phi > n0 || plo > phi || plo % 8 != 0 || (phi % 8 != 0 && phi != n0))
+      return fail(HJ_EINVAL, "plane range [%lld, %lld) must lie in [0, %lld) on multiples of 8 (or end at n[0])",
+                  (long long)plo, (long long)phi, (long long)n0);
+    if (plo == phi) return HJ_OK;
+  }
+  set_rows(P, w, part, plo, phi);
   rc = check_ham(ham, P.g.dim);
   if (rc) return rc;
   if (!alpha) return fail(HJ_EINVAL, "alpha is NULL");
@@ -305,11 +319,26 @@ int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double*
   return cuda_status(e, "hj_stage");
 }
 
+int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                  const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                  hj_stats* stats, int32_t tag, int part, void* stream) {
+  if (part < HJ_PART_ALL || part > HJ_PART_RIM) return fail(HJ_EINVAL, "unknown stage part %d", part);
+  return stage_impl(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, part, 0, 0,
+                    stream);
+}
+
+int hj_stage_planes(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                    const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                    hj_stats* stats, int32_t tag, int64_t plane_lo, int64_t plane_hi, void* stream) {
+  return stage_impl(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, STAGE_PLANES,
+                    plane_lo, plane_hi, stream);
+}
+
 int hj_stage(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
              const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
              hj_stats* stats, int32_t tag, void* stream) {
-  return hj_stage_part(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag,
-                       HJ_PART_ALL, stream);
+  return stage_impl(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, HJ_PART_ALL,
+                    0, 0, stream);
 }
 
 int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, const double* v,

@@ -287,10 +287,18 @@ def term_dev(dg: DeviceGrid, scheme: str, dh: DeviceHam, alphas, v: torch.Tensor
 def stage_dev(dg: DeviceGrid, scheme: str, dh: DeviceHam, alphas_c, dt: float, stage: int, y_in: torch.Tensor,
               y0: torch.Tensor | None, y_out: torch.Tensor, mask_prev: torch.Tensor | None = None,
               mask: int = 0, stats: Stats | None = None, tag: int = 0, lib=None, strm=None,
-              part: int = 0) -> None:
+              part: int = 0, planes: tuple[int, int] | None = None) -> None:
     """One fused TVD-RK stage (hj_stage; hj_stage_part when ``part`` is
     PART_CORE / PART_RIM).  ``alphas_c`` is a ctypes double[5]."""
     lib = lib or require()
+    if planes is not None:
+        rc = lib.hj_stage_planes(dg.ref, _lib.SCHEME_CODES[scheme], dh.ref, alphas_c, float(dt), int(stage),
+                                 ptr(y_in), ptr(y0), ptr(y_out), ptr(mask_prev), int(mask),
+                                 stats.p if stats else None, int(tag), int(planes[0]), int(planes[1]),
+                                 strm if strm is not None else stream())
+        if rc:
+            check(rc, "hj_stage_planes")
+        return
     if part:
         rc = lib.hj_stage_part(dg.ref, _lib.SCHEME_CODES[scheme], dh.ref, alphas_c, float(dt), int(stage),
                                ptr(y_in), ptr(y0), ptr(y_out), ptr(mask_prev), int(mask),

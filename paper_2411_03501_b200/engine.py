@@ -159,6 +159,105 @@ class FusedIntegrator:
             self._raise_pending(times, warn=zero_alpha)
         return DeviceIntegration(t, cur, steps, min_dt, max_dt)
 
+    # ------------------------------------------------------------ host -> host single step
+    # A call that takes one step on a host field (ode_cfl_k(..., single_step) or a
+    # span shorter than one CFL step) is copy-bound when run as H2D, stages,
+    # D2H.  The pipeline cuts the field into axis-0 chunks: the H2D of chunk
+    # k+1 (copy stream) overlaps the stages over the planes whose stencils are
+    # complete (hj_stage_planes; stage s lags stage s-1 by the ghost width,
+    # rounded to the kernels' 8-plane rows), and finished planes of the last
+    # stage go back to pinned host memory on a third stream.  The node updates
+    # are the same as one launch per stage, bit for bit.
+    pipeline_min_cells = 1 << 22     # smaller fields: plain copies are cheap
+    pipeline_chunk = 48              # planes per H2D chunk (multiple of 8; 48 measured best at 301^3)
+
+    def _pipeline_ok(self, opts, y_host: np.ndarray) -> bool:
+        # (a periodic first axis wraps the stencil of the first planes onto the
+        # last ones, which arrive last: no pipeline)
+        return (self._native_ok(opts) and self.dg.batch == 1 and y_host.size >= self.pipeline_min_cells
+                and self.g.counts[0] >= 16 and not self.g.is_periodic(0))
+
+    def integrate_host(self, order: int, tspan, y_host: np.ndarray, opts) -> tuple:
+        """_integrate on a host field; returns (t_final, y_host_final, steps, min_dt, max_dt)."""
+        t0, t1 = float(tspan[0]), float(tspan[1])
+        one_step = False
+        dt = 0.0
+        if t1 > t0 and self._pipeline_ok(opts, y_host):
+            bound = step_bound(self._alphas(t0, None), self.g)
+            dt = opts.cfl_factor * bound
+            if opts.max_step is not None:
+                dt = min(dt, opts.max_step)
+            last = dt >= t1 - t0
+            if last:
+                dt = t1 - t0
+            one_step = (opts.single_step or last) and dt > 0.0 and np.isfinite(dt)
+        if not one_step:
+            res = self.integrate(order, (t0, t1), dev.to_dev(y_host), opts)
+            return res.t_final, dev.to_host(res.y), res.steps_taken, res.min_dt, res.max_dt
+        t_next = t1 if dt >= t1 - t0 else t0 + dt
+        y_out = self._pipelined_step(order, t0, dt, y_host)
+        stage_t = (t0, t0 + dt, t0 + 0.5 * dt) if order == 3 else (t0, t0 + dt)
+        self._raise_pending({k: stage_t[k] for k in range(order)}, warn=bound == np.inf)
+        return t_next, y_out, 1, dt, dt
+
+    def _pipelined_step(self, order: int, t0: float, dt: float, y_host: np.ndarray) -> np.ndarray:
+        kinds = _STAGES[order]
+        n0 = self.g.counts[0]
+        w = 3                                        # widest ghost reach of any scheme
+        chunk = max(8, (int(self.pipeline_chunk) // 8) * 8)
+        first = min(chunk, 16)                       # a short first chunk starts the stages early
+        bounds = [min(first, n0)] + list(range(first + chunk, n0, chunk))
+        if bounds[-1] != n0:
+            bounds.append(n0)
+        shape = tuple(self.g.counts)
+        if getattr(self, "_pipe", None) is None or self._pipe[0] != shape:
+            mk = lambda: torch.empty(shape, dtype=dev.F64, device=dev.device())  # noqa: E731
+            self._pipe = (shape, [mk() for _ in range(len(kinds) + 1)], torch.cuda.Stream(), torch.cuda.Stream())
+        _, bufs, s_in, s_out = self._pipe
+        y_dev = bufs[0]
+        out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)
+        src_host = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
+        comp = torch.cuda.current_stream()
+        s_in.wait_stream(comp)                       # the buffers' previous users
+        s_out.wait_stream(comp)
+        alphas_c = _lib.doubles(self._alphas(t0, None), _lib.HJ_MAX_DIM)
+        self.stats.reset()
+        done = [0] * len(kinds)
+        arrived, nxt = 0, 0
+        drain = 16                                   # planes per launch once the input is complete
+        while done[-1] < n0:
+            if nxt < len(bounds):
+                b = bounds[nxt]
+                nxt += 1
+                with torch.cuda.stream(s_in):
+                    y_dev[arrived:b].copy_(src_host[arrived:b], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_in)
+                comp.wait_event(ev)
+                arrived = b
+            hi = arrived
+            for k, kind in enumerate(kinds):
+                # planes whose stencil inputs are complete: w behind the previous stage's front
+                hi = n0 if hi == n0 else max(0, ((hi - w) // 8) * 8)
+                if arrived == n0:
+                    hi = min(hi, done[k] + drain)    # drain in short pieces so the D2H starts early
+                if hi > done[k]:
+                    dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, bufs[k],
+                                  y_dev if kind != _lib.STAGE_EULER else None, bufs[k + 1], None, _lib.MASK_NONE,
+                                  self.stats, k, lib=self.lib, strm=comp.cuda_stream, planes=(done[k], hi))
+                    self.launches += 1
+                    if k == len(kinds) - 1:
+                        ev_o = torch.cuda.Event()
+                        ev_o.record(comp)
+                        s_out.wait_event(ev_o)
+                        with torch.cuda.stream(s_out):
+                            out_host[done[k]:hi].copy_(bufs[k + 1][done[k]:hi], non_blocking=True)
+                    done[k] = hi
+                hi = done[k]
+        s_out.synchronize()
+        comp.wait_stream(s_out)
+        return out_host.numpy()
+
     # ------------------------------------------------------------ native loop
     def _native_ok(self, opts) -> bool:
         """hj_integrate runs the whole loop in C++ when nothing needs the host

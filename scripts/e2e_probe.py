@@ -1,0 +1,39 @@
+"""Where the end-to-end (host field in, host field out) single RK3 step spends
+its time at 301^3: per-call setup, and the pipelined step per chunk size."""
+import time
+import numpy as np
+import torch
+
+import paper_2411_03501_b200 as hj
+from paper_2411_03501_b200.engine import FusedIntegrator
+
+g = hj.air3d_grid(301)
+cfg = hj.air3d_term_config(scheme="weno5")
+host = torch.empty(g.counts, dtype=torch.float64, pin_memory=True)
+host.copy_(torch.from_numpy(hj.cylinder(g, 2, (0.0, 0.0, 0.0), 5.0).values))
+y = host.numpy()
+opts = hj.IntegratorOptions(single_step=True)
+
+
+def t(fn, reps=5):
+    out = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        out.append(time.perf_counter() - t0)
+    return float(np.median(out)) * 1e3
+
+
+print("construct FusedIntegrator ms", t(lambda: FusedIntegrator(g, cfg)))
+fi = FusedIntegrator(g, cfg)
+fi.integrate_host(3, (0.0, 1.0), y, opts)
+for c in (16, 32, 48, 64, 96, 128):
+    fi.pipeline_chunk = c
+    print("chunk", c, "ms", t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts)), flush=True)
+fi.pipeline_min_cells = 1 << 40
+print("unpipelined ms", t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts)))
+rhs = hj.lax_friedrichs_rhs(g)
+yf = hj.ScalarField(y)
+print("public ode_cfl_3 ms", t(lambda: hj.ode_cfl_3(rhs, (0.0, 1.0), yf, opts, cfg)))
