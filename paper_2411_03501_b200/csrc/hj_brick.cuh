@@ -528,14 +528,15 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int SCHEME, int MINB, int UNR = 1>
+// UNR: walk unroll of the 3-D kernels; UNR4: of the 4-D kernels
+template <int SCHEME, int MINB, int UNR = 1, int UNR4 = UNR>
 static cudaError_t launch_brick_ham(const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = true;
   if (P.g.dim == 4) {
     if (!P.aux_p0 || !P.aux_d0) { *handled = false; return cudaSuccess; }
     switch (P.ham.kind) {
-      case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1, UNR>(P, s);
-      case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1, UNR>(P, s);
+      case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1, UNR4>(P, s);
+      case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1, UNR4>(P, s);
       default: *handled = false; return cudaSuccess;
     }
   }
