@@ -339,7 +339,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // behind the second/third-axis walks
   // (3-D only: the 4-D kernel has no registers to spare across the walks, it
   // reads them one node ahead inside the first-axis walk)
-  constexpr int QD = AO ? 1 : 2;
+  constexpr int QD = AO ? 1 : (SCHEME == HJ_WENO5_FMA ? 4 : 2);   // exact: more would spill
   const int cy = t / BYX, cx = t % BYX;
   const bool col_on = y0 + cy < n1 && x0 + cx < n2;
   const long long coff0 = (long long)z0 * s0 + (long long)(y0 + cy) * s1 + (x0 + cx);
