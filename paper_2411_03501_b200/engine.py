@@ -169,7 +169,7 @@ class FusedIntegrator:
     # stage go back to pinned host memory on a third stream.  The node updates
     # are the same as one launch per stage, bit for bit.
     pipeline_min_cells = 1 << 22     # smaller fields: plain copies are cheap
-    pipeline_chunk = 48              # planes per H2D chunk (multiple of 8; 48 measured best at 301^3)
+    pipeline_chunk = 32              # planes per H2D chunk (multiple of 8; 32 measured best at 301^3)
 
     def _pipeline_ok(self, opts, y_host: np.ndarray) -> bool:
         # (a periodic first axis wraps the stencil of the first planes onto the
@@ -212,28 +212,32 @@ class FusedIntegrator:
         shape = tuple(self.g.counts)
         if getattr(self, "_pipe", None) is None or self._pipe[0] != shape:
             mk = lambda: torch.empty(shape, dtype=dev.F64, device=dev.device())  # noqa: E731
-            self._pipe = (shape, [mk() for _ in range(len(kinds) + 1)], torch.cuda.Stream(), torch.cuda.Stream())
-        _, bufs, s_in, s_out = self._pipe
+            self._pipe = (shape, [mk() for _ in range(len(kinds) + 1)], torch.cuda.Stream(), torch.cuda.Stream(),
+                          [torch.cuda.Stream() for _ in kinds])
+        _, bufs, s_in, s_out, s_st = self._pipe
         y_dev = bufs[0]
         out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)
         src_host = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
         comp = torch.cuda.current_stream()
-        s_in.wait_stream(comp)                       # the buffers' previous users
-        s_out.wait_stream(comp)
+        for st in (s_in, s_out, *s_st):
+            st.wait_stream(comp)                     # the buffers' previous users
         alphas_c = _lib.doubles(self._alphas(t0, None), _lib.HJ_MAX_DIM)
         self.stats.reset()
         done = [0] * len(kinds)
         arrived, nxt = 0, 0
         drain = 16                                   # planes per launch once the input is complete
+        # one stream per stage: a stage's launch waits (events) for the input
+        # planes it reads, so launches of different stages overlap and fill
+        # each other's partial last waves
+        last_ev = [None] * (len(kinds) + 1)          # [0]: input chunks, [k+1]: stage k's latest launch
         while done[-1] < n0:
             if nxt < len(bounds):
                 b = bounds[nxt]
                 nxt += 1
                 with torch.cuda.stream(s_in):
                     y_dev[arrived:b].copy_(src_host[arrived:b], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(s_in)
-                comp.wait_event(ev)
+                    last_ev[0] = torch.cuda.Event()
+                    last_ev[0].record(s_in)
                 arrived = b
             hi = arrived
             for k, kind in enumerate(kinds):
@@ -242,20 +246,23 @@ class FusedIntegrator:
                 if arrived == n0:
                     hi = min(hi, done[k] + drain)    # drain in short pieces so the D2H starts early
                 if hi > done[k]:
+                    st = s_st[k]
+                    st.wait_event(last_ev[k])            # everything this launch reads has been produced
                     dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, bufs[k],
                                   y_dev if kind != _lib.STAGE_EULER else None, bufs[k + 1], None, _lib.MASK_NONE,
-                                  self.stats, k, lib=self.lib, strm=comp.cuda_stream, planes=(done[k], hi))
+                                  self.stats, k, lib=self.lib, strm=st.cuda_stream, planes=(done[k], hi))
                     self.launches += 1
+                    last_ev[k + 1] = torch.cuda.Event()
+                    last_ev[k + 1].record(st)
                     if k == len(kinds) - 1:
-                        ev_o = torch.cuda.Event()
-                        ev_o.record(comp)
-                        s_out.wait_event(ev_o)
+                        s_out.wait_event(last_ev[k + 1])
                         with torch.cuda.stream(s_out):
                             out_host[done[k]:hi].copy_(bufs[k + 1][done[k]:hi], non_blocking=True)
                     done[k] = hi
                 hi = done[k]
         s_out.synchronize()
-        comp.wait_stream(s_out)
+        for st in (s_in, s_out, *s_st):
+            comp.wait_stream(st)
         return out_host.numpy()
 
     # ------------------------------------------------------------ native loop
