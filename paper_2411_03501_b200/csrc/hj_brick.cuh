@@ -266,8 +266,15 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         if (r >= BZ) return S.zh[((r - BZ + HB) * BYX + y) * BYX + x];
         return S.v[r * PLANE + (y + HB) * SVP + (x + HB)];
       };
+      // (CTA-uniform / warp-uniform skips: which ghosts of this brick and plane
+      // are synthesised at all -- periodic and exchanged ones are already loaded)
+      const bool syn_y = (y0 < HB || y0 + BYX + HB > n1) && A1.bc != HJ_BC_PERIODIC;
+      const bool syn_x = (x0 < HB || x0 + BYX + HB > n2) && A2.bc != HJ_BC_PERIODIC;
+      const bool syn_zp = gz >= n0 && jz == GI_SYNTH;                       // this warp's plane
+      const bool syn_zh = ghost_index(A0, z0 - 1) == GI_SYNTH || ghost_index(A0, z0 + BZ) == GI_SYNTH ||
+                          ghost_index(A0, z0 + BZ + HB - 1) == GI_SYNTH;
       srow = &S.v[z * PLANE + lane];
-      for (int yy = 0; yy < SVR; ++yy, srow += SVP) {
+      for (int yy = 0; yy < SVR && (syn_y || syn_x || syn_zp); ++yy, srow += SVP) {
         const bool yin = yy >= HB && yy < HB + BYX;
         if (!lane_on || !(yin || xin)) continue;
         const int gy = y0 + yy - HB;
@@ -292,7 +299,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         }
       }
 #pragma unroll
-      for (int r2 = warp; r2 < HB * BYX; r2 += BRICK_THREADS / 32) {
+      for (int r2 = warp; r2 < HB * BYX && syn_zh; r2 += BRICK_THREADS / 32) {
         const int row = 2 * r2 + half;
         const int k = row / BYX, y = row % BYX;
         const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
