@@ -203,12 +203,6 @@ class FusedIntegrator:
     def _pipelined_step(self, order: int, t0: float, dt: float, y_host: np.ndarray) -> np.ndarray:
         kinds = _STAGES[order]
         n0 = self.g.counts[0]
-        w = 3                                        # widest ghost reach of any scheme
-        chunk = max(8, (int(self.pipeline_chunk) // 8) * 8)
-        first = min(chunk, 16)                       # a short first chunk starts the stages early
-        bounds = [min(first, n0)] + list(range(first + chunk, n0, chunk))
-        if bounds[-1] != n0:
-            bounds.append(n0)
         shape = tuple(self.g.counts)
         if getattr(self, "_pipe", None) is None or self._pipe[0] != shape:
             mk = lambda: torch.empty(shape, dtype=dev.F64, device=dev.device())  # noqa: E731
@@ -223,43 +217,30 @@ class FusedIntegrator:
             st.wait_stream(comp)                     # the buffers' previous users
         alphas_c = _lib.doubles(self._alphas(t0, None), _lib.HJ_MAX_DIM)
         self.stats.reset()
-        done = [0] * len(kinds)
-        arrived, nxt = 0, 0
-        drain = 16                                   # planes per launch once the input is complete
-        # one stream per stage: a stage's launch waits (events) for the input
-        # planes it reads, so launches of different stages overlap and fill
-        # each other's partial last waves
+        # one stream per stage: a launch waits (events) for the latest launch of
+        # the stage before it (or the latest input chunk), so launches of
+        # different stages overlap and fill each other's partial last waves
         last_ev = [None] * (len(kinds) + 1)          # [0]: input chunks, [k+1]: stage k's latest launch
-        while done[-1] < n0:
-            if nxt < len(bounds):
-                b = bounds[nxt]
-                nxt += 1
+        for op, k, lo, hi in pipeline_plan(n0, len(kinds), int(self.pipeline_chunk)):
+            if op == "h2d":
                 with torch.cuda.stream(s_in):
-                    y_dev[arrived:b].copy_(src_host[arrived:b], non_blocking=True)
+                    y_dev[lo:hi].copy_(src_host[lo:hi], non_blocking=True)
                     last_ev[0] = torch.cuda.Event()
                     last_ev[0].record(s_in)
-                arrived = b
-            hi = arrived
-            for k, kind in enumerate(kinds):
-                # planes whose stencil inputs are complete: w behind the previous stage's front
-                hi = n0 if hi == n0 else max(0, ((hi - w) // 8) * 8)
-                if arrived == n0:
-                    hi = min(hi, done[k] + drain)    # drain in short pieces so the D2H starts early
-                if hi > done[k]:
-                    st = s_st[k]
-                    st.wait_event(last_ev[k])            # everything this launch reads has been produced
-                    dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, bufs[k],
-                                  y_dev if kind != _lib.STAGE_EULER else None, bufs[k + 1], None, _lib.MASK_NONE,
-                                  self.stats, k, lib=self.lib, strm=st.cuda_stream, planes=(done[k], hi))
-                    self.launches += 1
-                    last_ev[k + 1] = torch.cuda.Event()
-                    last_ev[k + 1].record(st)
-                    if k == len(kinds) - 1:
-                        s_out.wait_event(last_ev[k + 1])
-                        with torch.cuda.stream(s_out):
-                            out_host[done[k]:hi].copy_(bufs[k + 1][done[k]:hi], non_blocking=True)
-                    done[k] = hi
-                hi = done[k]
+            elif op == "stage":
+                st = s_st[k]
+                st.wait_event(last_ev[k])            # everything this launch reads has been produced
+                kind = kinds[k]
+                dev.stage_dev(self.dg, self.scheme, self.dh, alphas_c, dt, kind, bufs[k],
+                              y_dev if kind != _lib.STAGE_EULER else None, bufs[k + 1], None, _lib.MASK_NONE,
+                              self.stats, k, lib=self.lib, strm=st.cuda_stream, planes=(lo, hi))
+                self.launches += 1
+                last_ev[k + 1] = torch.cuda.Event()
+                last_ev[k + 1].record(st)
+            else:   # "d2h" of finished planes of the last stage
+                s_out.wait_event(last_ev[-1])
+                with torch.cuda.stream(s_out):
+                    out_host[lo:hi].copy_(bufs[-1][lo:hi], non_blocking=True)
         s_out.synchronize()
         for st in (s_in, s_out, *s_st):
             comp.wait_stream(st)
@@ -371,6 +352,44 @@ class FusedIntegrator:
         except ValueError as err:
             # integrator.py:61-63
             raise RuntimeError(f"term evaluation failed at step {step} (t={t:g}): {err}") from err
+
+
+def pipeline_plan(n0: int, stages: int, chunk: int, reach: int = 3, row: int = 8, first: int = 16,
+                  drain: int = 16) -> list[tuple[str, int, int, int]]:
+    """Schedule of the pipelined host->host step over axis-0 planes [0, n0):
+    ("h2d", -1, lo, hi) input chunks (a short first chunk, then ``chunk``
+    planes), ("stage", k, lo, hi) launches of stage k over planes whose
+    stencil inputs are complete -- ``reach`` planes behind the previous
+    stage's front (or its end), rounded down to the kernels' ``row``-plane
+    rows -- and ("d2h", -1, lo, hi) copies of the last stage's finished
+    planes.  Once the whole input has arrived every stage advances by at most
+    ``drain`` planes per round, so the final copies start early.  Pure host
+    logic (tests/test_host_logic.py checks coverage and dependencies)."""
+    chunk = max(row, (chunk // row) * row)
+    first = min(chunk, first)
+    bounds = [min(first, n0)] + list(range(first + chunk, n0, chunk))
+    if bounds[-1] != n0:
+        bounds.append(n0)
+    plan: list[tuple[str, int, int, int]] = []
+    done = [0] * stages
+    arrived, nxt = 0, 0
+    while done[-1] < n0:
+        if nxt < len(bounds):
+            plan.append(("h2d", -1, arrived, bounds[nxt]))
+            arrived = bounds[nxt]
+            nxt += 1
+        hi = arrived
+        for k in range(stages):
+            hi = n0 if hi == n0 else max(0, ((hi - reach) // row) * row)
+            if arrived == n0:
+                hi = min(hi, done[k] + drain)
+            if hi > done[k]:
+                plan.append(("stage", k, done[k], hi))
+                if k == stages - 1:
+                    plan.append(("d2h", -1, done[k], hi))
+                done[k] = hi
+            hi = done[k]
+    return plan
 
 
 def integrate_fused(g, cfg: TermConfig, order: int, tspan, y0_host: np.ndarray, opts) -> DeviceIntegration:

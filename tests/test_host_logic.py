@@ -171,3 +171,45 @@ def test_reference_names_exported():
             if isinstance(node, ast.Assign) and node.targets[0].id == "__all__":
                 ref_all = [e.value for e in node.value.elts]
         assert sorted(ref_all) == sorted(hj.REFERENCE_ALL)
+
+
+# ---------------------------------------------------------------- pipelined host->host step (engine.pipeline_plan)
+@pytest.mark.parametrize("n0", [16, 17, 40, 61, 301, 801])
+@pytest.mark.parametrize("stages", [1, 2, 3])
+@pytest.mark.parametrize("chunk", [8, 32, 48, 64])
+def test_pipeline_plan_covers_and_respects_dependencies(n0, stages, chunk):
+    from paper_2411_03501_b200.engine import pipeline_plan
+
+    plan = pipeline_plan(n0, stages, chunk)
+    arrived = 0
+    done = [0] * stages
+    copied = 0
+    for op, k, lo, hi in plan:
+        assert lo < hi
+        if op == "h2d":
+            assert lo == arrived
+            arrived = hi
+        elif op == "stage":
+            assert lo == done[k] and lo % 8 == 0 and (hi % 8 == 0 or hi == n0)
+            src_front = arrived if k == 0 else done[k - 1]
+            # the launch reads planes [lo-3, hi+3) of its input: all produced
+            # (beyond n0 they are boundary ghosts of a complete input)
+            assert src_front == n0 or hi + 3 <= src_front
+            done[k] = hi
+        else:
+            assert op == "d2h" and lo == copied and hi <= done[-1]
+            copied = hi
+    assert arrived == n0 and done == [n0] * stages and copied == n0
+
+
+def test_compute_api_fails_loudly_without_cuda():
+    """No CPU fallback: without a GPU every compute entry point raises."""
+    import torch
+
+    import paper_2411_03501_b200 as hj
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    g = hj.create_grid((0.0,), (1.0,), (16,))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        hj.upwind_first_weno5(g, hj.ScalarField(np.linspace(0.0, 1.0, 16)), 0)
