@@ -90,6 +90,48 @@ def steps_rate(g, cfg, y, k=5, w=2, dg=None):
     return s.elapsed_time(e) / 1e3 / k
 
 
+def c3(scheme="weno5"):
+    """C3 Air3D 801^3: one-GPU RK3 steps, and the slab split for 2/4/8 ranks
+    emulated on this one GPU (every slab's overlapped core/rim stages run in
+    turn, halos copied between stages -- compute only, no NVLink traffic):
+    per-rank step time = total / P."""
+    from paper_2411_03501_b200.distributed import LocalTransport, SlabIntegrator, lockstep_step3, partition
+
+    n = int(os.environ.get("C3_N", "801"))
+    g = hj.air3d_grid(n)
+    cfg = hj.air3d_term_config(scheme=scheme)
+    dg = dev.device_grid(g)
+    y = dev.init_shape_dev(dg, _lib.SHAPE_CYLINDER, [0.0, 0.0, 0.0, 5.0, 4.0])
+    sec1 = steps_rate(g, cfg, y, k=3, w=1)
+    out = {"config": f"C3 Air3D {n}^3 WENO5+LF+RK3", "scheme": scheme, "ms_per_rk3_step_1gpu": sec1 * 1e3,
+           "cell_updates_per_s_1gpu": n ** 3 * 3 / sec1}
+    y_host = dev.to_host(y)
+    del y
+    alphas = cfg.partials.alphas(0.0, g)
+    dt = 0.5 / float(np.sum(alphas / g.spacings))
+    emu = {}
+    for world in (2, 4, 8):
+        slabs = partition(n, world, 3, False)
+        hub = LocalTransport(slabs)
+        runs = [SlabIntegrator(g, cfg, r, world, transport=hub.for_rank(r)) for r in range(world)]
+        ys = [run.scatter(y_host) for run in runs]
+        ys = lockstep_step3(runs, hub, ys, 0.0, dt)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(2):
+            ys = lockstep_step3(runs, hub, ys, 0.0, dt)
+        e.record()
+        torch.cuda.synchronize()
+        per_rank = s.elapsed_time(e) / 2 / world
+        emu[str(world)] = {"ms_per_rk3_step_per_rank": per_rank,
+                           "compute_only_strong_scaling_eff": sec1 * 1e3 / (world * per_rank)}
+        del runs, ys, hub
+        torch.cuda.empty_cache()
+    out["slab_emulation_1gpu"] = emu
+    return out
+
+
 def c4(scheme="weno5"):
     n = int(os.environ.get("C4_N", "121"))
     g = hj.di4_grid(n)
