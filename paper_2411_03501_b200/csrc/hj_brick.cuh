@@ -427,10 +427,20 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       };
       auto emit = [&](int i, double L, double R) {
         if (i >= zmax) return;
-        const double yz = qy[0], pv = nz_m, a0 = nz_p0, d0 = nz_d0;
-#pragma unroll
-        for (int k = 0; k + 1 < QD; ++k) qy[k] = qy[k + 1];
-        qy[QD - 1] = (need_y0 && i + QD < zmax && i + QD < BZ) ? y0p[off0 + (long long)(i + QD) * s0] : 0.0;
+        // node i's y0 sits in slot i % QD; the slot is refilled with node i+QD.
+        // (A shift queue would move the youngest, still-loading slot every
+        // node and stall on it; the uniform switch touches one slot only.)
+        double yz = 0.0;
+        const bool refill = need_y0 && i + QD < zmax && i + QD < BZ;
+        const double* nxt_y0 = y0p + (off0 + (long long)(i + QD) * s0);
+        switch (i % QD) {
+          case 0: yz = qy[0]; if (refill) qy[0] = *nxt_y0; break;
+          case 1: if constexpr (QD > 1) { yz = qy[QD > 1 ? 1 : 0]; if (refill) qy[QD > 1 ? 1 : 0] = *nxt_y0; } break;
+          case 2: if constexpr (QD > 2) { yz = qy[QD > 2 ? 2 : 0]; if (refill) qy[QD > 2 ? 2 : 0] = *nxt_y0; } break;
+          default: if constexpr (QD > 3) { yz = qy[QD - 1]; if (refill) qy[QD - 1] = *nxt_y0; } break;
+        }
+        static_assert(QD >= 1 && QD <= 4, "y0 prefetch depth 1..4");
+        const double pv = nz_m, a0 = nz_p0, d0 = nz_d0;
         if (i + 1 < zmax && i + 1 < BZ) fetch_node(i + 1);
         const int s = s00 + i * (BYX * BYX);
         double p[3 + AO];
