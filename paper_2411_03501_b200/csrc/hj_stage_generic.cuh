@@ -26,16 +26,28 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
   if (idx < total && P.zp.has(ix[0])) {
     double pbar[DIM];
     double diss = 0.0;
+    // every stencil value of every axis first: a node whose stencils stay
+    // inside the owned block takes them with plain loads, all in flight at
+    // once (small grids are latency-bound); other nodes go through fetch()
+    bool inner = true;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) inner = inner && ix[a] >= W && ix[a] < P.g.ax[a].n - W;
+    double uu[DIM][7];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
       const AxisView& A = P.g.ax[a];
       const double* line = P.y_in + (off - (long long)ix[a] * A.stride);
-      double u[7];
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
-        if (k >= 3 - W && k <= 3 + W) u[k] = fetch(line, A, ix[a] - 3 + k);
-        else u[k] = 0.0;
+        if (k >= 3 - W && k <= 3 + W)
+          uu[a][k] = inner ? line[(long long)(ix[a] - 3 + k) * A.stride] : fetch(line, A, ix[a] - 3 + k);
+        else
+          uu[a][k] = 0.0;
       }
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double* u = uu[a];
       const LR lr = scheme_lr<SCHEME>(u, P.g.sp[a], P.eps_mode);
       if (!finite(lr.l) || !finite(lr.r)) flags |= HJ_NF_DERIV;
       if (P.want_ranges) {
