@@ -1,4 +1,10 @@
 """C1: host issue time of one interval's native stage loop vs its device time."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import time
 import numpy as np
 import torch

@@ -1,5 +1,11 @@
 """Where the end-to-end (host field in, host field out) single RK3 step spends
 its time at 301^3: per-call setup, and the pipelined step per chunk size."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import time
 import numpy as np
 import torch

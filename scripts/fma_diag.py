@@ -1,6 +1,12 @@
 """Conditioning probe for the tolerance-mode WENO5: full-horizon Air3D tubes,
 exact vs fma vs exact with a 1-ulp perturbed target; per-snapshot L-inf rel
 and where the largest difference sits."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import sys
 import numpy as np
 import paper_2411_03501_b200 as hj
