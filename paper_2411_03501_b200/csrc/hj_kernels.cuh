@@ -53,6 +53,19 @@ struct StageArgs {
 // Split a linear owned-node index into (problem, per-axis indices) and the
 // element offset of that node from the problem-0 base pointer.
 __device__ __forceinline__ long long locate(const GridArgs& g, long long idx, int* ix) {
+  if (idx < (1LL << 31)) {
+    // 32-bit index arithmetic (a 64-bit division is ~100 instructions; small
+    // grids are instruction-bound on exactly this)
+    unsigned rem = (unsigned)idx;
+    long long off = 0;
+    for (int a = g.dim - 1; a >= 0; --a) {
+      const unsigned q = rem / (unsigned)g.n[a];
+      ix[a] = (int)(rem - q * (unsigned)g.n[a]);
+      off += (long long)ix[a] * g.stride[a];
+      rem = q;
+    }
+    return off + (long long)rem * g.batch_stride;
+  }
   long long rem = idx;
   long long off = 0;
   for (int a = g.dim - 1; a >= 0; --a) {
