@@ -450,10 +450,8 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         p[AO + 2] = S.p2[s];
         // derivative / p_avg finiteness, as ScalarField(p_avg) checks it (term.py:101):
         // a non-finite one-sided derivative always makes its p_avg non-finite
-        unsigned nf = 0u;
-#pragma unroll
-        for (int a = 0; a < 3 + AO; ++a) nf |= ((abs_hi(p[a]) | 0x000FFFFFu) >= 0x7FFFFFFFu) ? 1u : 0u;
-        if (nf) flags |= HJ_NF_DERIV;
+        // (tested below together with the node's other values: one compare on the
+        // largest exponent field, the per-class flags only on the rare failure)
         // AO = 1: the dissipation continues from the axis-0 pre-pass
         const double dsum = (((AO ? d0 : 0.0) + ah * (R - L)) + S.t1[s]) + S.t2[s];
         // ham_eval inputs (hj_ham.cuh): 3-D Hamiltonians take the axis-0/1 nodes
@@ -470,17 +468,27 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
           ham_inputs<HAM, 4>(P.ham, G.nodes, ix, cin);
         }
         const double H = ham_eval<HAM, 3 + AO>(P.ham, cin, p);
-        if (!finite(H)) flags |= HJ_NF_HAM;
         if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
         const double delta = dsum - H;                           // term.py:113
-        if (!finite(delta)) flags |= HJ_NF_DELTA;
         const double yv = col[i * PLANE];
-        if (!finite(yv)) flags |= HJ_NF_INPUT;
         double o = stage_update(P.stage, P.dt, yv, yz, delta);
         if (P.mask == HJ_MASK_MIN) o = (pv < o) ? pv : o;
         else if (P.mask == HJ_MASK_MAX) o = (pv > o) ? pv : o;
-        if (!finite(o)) flags |= HJ_NF_OUTPUT;
         out[off0 + (long long)i * s0] = o;
+        // non-finite flags: finite(x) <=> |hi(x)| < 0x7FF00000
+        unsigned big = max(max(abs_hi(H), abs_hi(delta)), max(abs_hi(yv), abs_hi(o)));
+#pragma unroll
+        for (int a = 0; a < 3 + AO; ++a) big = max(big, abs_hi(p[a]));
+        if (big >= 0x7FF00000u) {
+          unsigned nf = 0u;
+#pragma unroll
+          for (int a = 0; a < 3 + AO; ++a) nf |= (abs_hi(p[a]) >= 0x7FF00000u) ? 1u : 0u;
+          if (nf) flags |= HJ_NF_DERIV;
+          if (!finite(H)) flags |= HJ_NF_HAM;
+          if (!finite(delta)) flags |= HJ_NF_DELTA;
+          if (!finite(yv)) flags |= HJ_NF_INPUT;
+          if (!finite(o)) flags |= HJ_NF_OUTPUT;
+        }
       };
       line_walk<SCHEME, WALK_UNROLL, SEG>(ld, G.sp[AO], emit);
     }
