@@ -169,7 +169,8 @@ class FusedIntegrator:
     # stage go back to pinned host memory on a third stream.  The node updates
     # are the same as one launch per stage, bit for bit.
     pipeline_min_cells = 1 << 22     # smaller fields: plain copies are cheap
-    pipeline_chunk = 32              # planes per H2D chunk (multiple of 8; 32 measured best at 301^3)
+    pipeline_chunk = 16              # planes per H2D chunk (multiple of 8; 16 measured best at 301^3, scripts/e2e_probe.py)
+    pipeline_priority = True         # later RK stages on higher-priority streams (the D2H-feeding stage first)
 
     def _pipeline_ok(self, opts, y_host: np.ndarray) -> bool:
         # (a periodic first axis wraps the stencil of the first planes onto the
@@ -204,10 +205,15 @@ class FusedIntegrator:
         kinds = _STAGES[order]
         n0 = self.g.counts[0]
         shape = tuple(self.g.counts)
-        if getattr(self, "_pipe", None) is None or self._pipe[0] != shape:
+        prio = bool(self.pipeline_priority)
+        if getattr(self, "_pipe", None) is None or self._pipe[0] != (shape, prio):
             mk = lambda: torch.empty(shape, dtype=dev.F64, device=dev.device())  # noqa: E731
-            self._pipe = (shape, [mk() for _ in range(len(kinds) + 1)], torch.cuda.Stream(), torch.cuda.Stream(),
-                          [torch.cuda.Stream() for _ in kinds])
+            # stage k on priority -k: when launches of several stages are ready
+            # the block scheduler serves the later stage first, so the last
+            # stage (and its D2H) trails the input by as little as possible
+            self._pipe = ((shape, prio), [mk() for _ in range(len(kinds) + 1)], torch.cuda.Stream(),
+                          torch.cuda.Stream(), [torch.cuda.Stream(priority=-k if prio else 0)
+                                                for k in range(len(kinds))])
         _, bufs, s_in, s_out, s_st = self._pipe
         y_dev = bufs[0]
         out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)

@@ -1,5 +1,6 @@
 """Where the end-to-end (host field in, host field out) single RK3 step spends
-its time at 301^3: per-call setup, and the pipelined step per chunk size."""
+its time at 301^3: per-call setup, and the pipelined step per chunk size and
+stream-priority setting."""
 import os
 import sys
 
@@ -35,9 +36,14 @@ def t(fn, reps=5):
 print("construct FusedIntegrator ms", t(lambda: FusedIntegrator(g, cfg)))
 fi = FusedIntegrator(g, cfg)
 fi.integrate_host(3, (0.0, 1.0), y, opts)
-for c in (16, 32, 48, 64, 96, 128):
-    fi.pipeline_chunk = c
-    print("chunk", c, "ms", t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts)), flush=True)
+ref = fi.integrate_host(3, (0.0, 1.0), y, opts)[1].copy()
+for prio in (False, True):
+    fi.pipeline_priority = prio
+    for c in (8, 16, 24, 32):
+        fi.pipeline_chunk = c
+        same = np.array_equal(fi.integrate_host(3, (0.0, 1.0), y, opts)[1], ref)
+        print("priority", prio, "chunk", c, "ms", t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts), reps=9),
+              "bit-identical", same, flush=True)
 fi.pipeline_min_cells = 1 << 40
 print("unpipelined ms", t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts)))
 rhs = hj.lax_friedrichs_rhs(g)

@@ -13,10 +13,12 @@ from paper_2411_03501_b200.engine import FusedIntegrator
 pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("stage_kernel")]
 
 
-@pytest.fixture
-def small_pipeline(monkeypatch):
+@pytest.fixture(params=[(16, True), (8, False)], ids=["chunk16-prio", "chunk8-noprio"])
+def small_pipeline(monkeypatch, request):
+    chunk, prio = request.param
     monkeypatch.setattr(FusedIntegrator, "pipeline_min_cells", 0)
-    monkeypatch.setattr(FusedIntegrator, "pipeline_chunk", 16)
+    monkeypatch.setattr(FusedIntegrator, "pipeline_chunk", chunk)
+    monkeypatch.setattr(FusedIntegrator, "pipeline_priority", prio)
 
 
 def _both(g, cfg, y0, order, opts):

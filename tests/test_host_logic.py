@@ -176,7 +176,7 @@ def test_reference_names_exported():
 # ---------------------------------------------------------------- pipelined host->host step (engine.pipeline_plan)
 @pytest.mark.parametrize("n0", [16, 17, 40, 61, 301, 801])
 @pytest.mark.parametrize("stages", [1, 2, 3])
-@pytest.mark.parametrize("chunk", [8, 32, 48, 64])
+@pytest.mark.parametrize("chunk", [8, 16, 32, 48, 64])
 def test_pipeline_plan_covers_and_respects_dependencies(n0, stages, chunk):
     from paper_2411_03501_b200.engine import pipeline_plan
 
