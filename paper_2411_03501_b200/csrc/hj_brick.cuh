@@ -363,8 +363,12 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // ---- second and third brick axes together: warps 0-3 walk the BZ x BYX
   // lines along y, warps 4-7 the lines along x, each a whole 16-node edge;
   // they leave p_avg and the dissipation term of their axis per node
+  // (lines whose nodes all lie outside the domain -- the partial bricks at
+  // the far faces -- are skipped: nothing reads their p_avg / dissipation,
+  // and the FP64 pipe they would occupy is shared with the SM's other warps)
   if (t < BRICK_THREADS / 2) {
     const int x = t % BYX, z = t / BYX;
+    if (z0 + z < n0 && x0 + x < n2) {
     const double* line = &S.v[z * PLANE + HB * SVP + (x + HB)];
     const double ah = P.alpha_half[AO + 1];
     auto ld = [&](int k) -> double { return line[k * SVP]; };
@@ -374,8 +378,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       S.t1[s] = ah * (R - L);                                // term.py:85-86
     };
     line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit);
+    }
   } else {
     const int y = t % BYX, z = (t - BRICK_THREADS / 2) / BYX;
+    if (z0 + z < n0 && y0 + y < n1) {
     const double* line = &S.v[z * PLANE + (y + HB) * SVP + HB];
     const double ah = P.alpha_half[AO + 2];
     const int row = (z * BYX + y) * BYX;
@@ -386,6 +392,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       S.t2[s] = ah * (R - L);
     };
     line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit);
+    }
   }
   __syncthreads();
 
