@@ -171,6 +171,8 @@ class FusedIntegrator:
     pipeline_min_cells = 1 << 22     # smaller fields: plain copies are cheap
     pipeline_chunk = 16              # planes per H2D chunk (multiple of 8; 16 measured best at 301^3, scripts/e2e_probe.py)
     pipeline_priority = True         # later RK stages on higher-priority streams (the D2H-feeding stage first)
+    pipeline_first = 16              # planes of the first H2D chunk
+    pipeline_drain = 16              # planes per stage launch once the whole input has arrived
 
     def _pipeline_ok(self, opts, y_host: np.ndarray) -> bool:
         # (a periodic first axis wraps the stencil of the first planes onto the
@@ -227,7 +229,8 @@ class FusedIntegrator:
         # the stage before it (or the latest input chunk), so launches of
         # different stages overlap and fill each other's partial last waves
         last_ev = [None] * (len(kinds) + 1)          # [0]: input chunks, [k+1]: stage k's latest launch
-        for op, k, lo, hi in pipeline_plan(n0, len(kinds), int(self.pipeline_chunk)):
+        for op, k, lo, hi in pipeline_plan(n0, len(kinds), int(self.pipeline_chunk),
+                                          first=int(self.pipeline_first), drain=int(self.pipeline_drain)):
             if op == "h2d":
                 with torch.cuda.stream(s_in):
                     y_dev[lo:hi].copy_(src_host[lo:hi], non_blocking=True)

@@ -37,6 +37,14 @@ print("construct FusedIntegrator ms", t(lambda: FusedIntegrator(g, cfg)))
 fi = FusedIntegrator(g, cfg)
 fi.integrate_host(3, (0.0, 1.0), y, opts)
 ref = fi.integrate_host(3, (0.0, 1.0), y, opts)[1].copy()
+fi.pipeline_chunk = 16
+for first in (8, 16):
+    for drain in (8, 16, 32):
+        fi.pipeline_first, fi.pipeline_drain = first, drain
+        same = np.array_equal(fi.integrate_host(3, (0.0, 1.0), y, opts)[1], ref)
+        print("chunk 16 first", first, "drain", drain, "ms",
+              t(lambda: fi.integrate_host(3, (0.0, 1.0), y, opts), reps=9), "bit-identical", same, flush=True)
+fi.pipeline_first, fi.pipeline_drain = 16, 16
 for prio in (False, True):
     fi.pipeline_priority = prio
     for c in (8, 16, 24, 32):

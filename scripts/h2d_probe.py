@@ -32,4 +32,22 @@ res = {
     "host_copy_into_pinned_numpy": gb / t(lambda: np.copyto(pin.numpy(), a)),
     "torch_threads": torch.get_num_threads(),
 }
+
+# both directions at once (the pipelined host->host step overlaps them):
+# seconds for one field each way, on two copy streams
+d2 = torch.empty_like(d)
+pin2 = torch.empty(n, dtype=torch.float64, pin_memory=True)
+s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def both():
+    with torch.cuda.stream(s_in):
+        d.copy_(pin, non_blocking=True)
+    with torch.cuda.stream(s_out):
+        pin2.copy_(d2, non_blocking=True)
+    s_in.synchronize()
+    s_out.synchronize()
+
+
+res["bidirectional_each_way"] = gb / t(both)
 print({k: round(v, 2) if isinstance(v, float) else v for k, v in res.items()}, "GB/s")
