@@ -38,6 +38,7 @@ enum {
   HJ_OK = 0,
   HJ_EINVAL = -1,     /* argument validation (reference: ValueError)           */
   HJ_ECUDA = -2,      /* CUDA launch / runtime failure                         */
+  HJ_ENCCL = -3,      /* NCCL missing or failed (multi-GPU hj_dd_* calls)      */
   HJ_ENONFINITE = -4  /* reserved: non-finite data (reported through hj_stats) */
 };
 
@@ -112,6 +113,10 @@ enum {
  * front of / behind the owned planes and the kernels read them instead of
  * synthesising boundary ghosts; field pointers always point at the first
  * OWNED plane. */
+/* exchanged halo planes per side a slab buffer must carry (hj_grid.halo):
+ * the fused stage kernels stage this many whatever the scheme's ghost width */
+#define HJ_HALO_MIN 3
+
 typedef struct hj_grid {
   int32_t dim;                        /* 1..4 (HJ_MAX_DIM reserved)                         */
   int32_t batch;                      /* >= 1 independent problems stacked in front         */
@@ -270,6 +275,47 @@ int hj_set_stage_kernel(int variant);
 int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream);
 /* zero a device hj_stats (keys set to +inf/-inf images) */
 int hj_stats_reset(hj_stats* stats, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU slabs
+ * Axis 0 split into contiguous slabs, one rank (process, GPU) each; the
+ * field buffer of a slab carries hj_grid.halo (>= HJ_HALO_MIN) exchanged
+ * planes in front of / behind its owned planes, and field pointers point at
+ * the first owned plane.  NCCL is resolved at run time (dlopen libnccl.so.2,
+ * or $HJ_NCCL_LIB); every call is stream-ordered, none synchronises the host.
+ * Reference: the per-interval loop of reachability.py:242-249 with the ghost
+ * extension of grid.py:203-225 along axis 0 replaced by the neighbours' planes
+ * (halo depth = GHOST_WIDTH, spatial.py:27). */
+#define HJ_DD_UID_BYTES 128
+typedef struct hj_dd hj_dd;   /* opaque: communicator, exchange stream, events */
+/* NCCL version code of the loaded library (>0) or HJ_ENCCL */
+int hj_dd_nccl_version(void);
+/* ncclGetUniqueId on the root rank; the host broadcasts the HJ_DD_UID_BYTES */
+int hj_dd_unique_id(void* uid);
+/* ncclCommInitRank on the current CUDA device; lo_rank / hi_rank = the axis-0
+ * neighbours (-1 at a global edge; a periodic axis 0 makes a ring, a
+ * one-rank ring exchanges with itself) */
+int hj_dd_init(const void* uid, int nranks, int rank, int lo_rank, int hi_rank, hj_dd** dd);
+/* One fused stage of this rank's slab (arguments as hj_stage): grouped
+ * ncclSend/ncclRecv of the halo planes of y_in with both neighbours on the
+ * communicator's stream, the CORE part on `stream` meanwhile (overlap != 0),
+ * `stream` waits on the exchange, then the RIM part.  Bit-identical to the
+ * undecomposed stage. */
+int hj_dd_stage(hj_dd* dd, const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt,
+                int stage, const double* y_in, const double* y0, double* y_out, const double* mask_prev,
+                int mask, hj_stats* stats, int32_t tag, int overlap, void* stream);
+/* halo exchange of buf alone, `stream` ordered after it */
+int hj_dd_exchange(hj_dd* dd, const hj_grid* g, double* buf, void* stream);
+/* all-reduce a device hj_stats across the ranks: lo_key min, hi_key max,
+ * nonfinite OR, first_bad_tag min -- every rank then holds the single-GPU run's
+ * stats (the first failing stage and error class, the global costate ranges) */
+int hj_dd_reduce_stats(hj_dd* dd, hj_stats* stats, void* stream);
+/* gather every rank's owned planes (count doubles) into `full` on rank root,
+ * in rank order; counts (host, nranks entries) are needed on the root only */
+int hj_dd_gather(hj_dd* dd, const double* owned, int64_t count, double* full, const int64_t* counts, int root,
+                 void* stream);
+/* exchanges posted and halo bytes sent by this rank so far */
+int hj_dd_stats(const hj_dd* dd, uint64_t* exchanges, uint64_t* halo_bytes);
+int hj_dd_free(hj_dd* dd);
 
 #ifdef __cplusplus
 }

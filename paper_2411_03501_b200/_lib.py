@@ -30,6 +30,9 @@ NF_INPUT, NF_DERIV, NF_HAM, NF_DELTA, NF_OUTPUT = 1, 2, 4, 8, 16
 FLAG_HAM_NONZERO = 32
 NF_MASK = 31
 PART_ALL, PART_CORE, PART_RIM = range(3)   # hj_stage_part (hjb200.h HJ_PART_*)
+HALO_MIN = 3          # hjb200.h HJ_HALO_MIN: exchanged planes per side of a slab buffer
+DD_UID_BYTES = 128    # hjb200.h HJ_DD_UID_BYTES
+HJ_ENCCL = -3
 
 
 class HjGrid(ctypes.Structure):
@@ -109,6 +112,17 @@ _SIGNATURES = [
     ("hj_set_stage_kernel", c_int, [c_int]),
     ("hj_divided_differences", c_int, [POINTER(HjGrid), c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p]),
+    # multi-GPU slabs (hj_dd.cu)
+    ("hj_dd_nccl_version", c_int, []),
+    ("hj_dd_unique_id", c_int, [c_void_p]),
+    ("hj_dd_init", c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
+    ("hj_dd_stage", c_int, [c_void_p, POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_double, c_int,
+                            c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int32, c_int, c_void_p]),
+    ("hj_dd_exchange", c_int, [c_void_p, POINTER(HjGrid), c_void_p, c_void_p]),
+    ("hj_dd_reduce_stats", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("hj_dd_gather", c_int, [c_void_p, c_void_p, c_int64, c_void_p, POINTER(c_int64), c_int, c_void_p]),
+    ("hj_dd_stats", c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    ("hj_dd_free", c_int, [c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)
@@ -149,6 +163,8 @@ def check(rc: int, what: str) -> None:
     msg = (load().hj_last_error() or b"").decode()
     if rc == HJ_EINVAL:
         raise ValueError(msg or f"{what}: invalid argument")
+    if rc == HJ_ENCCL:
+        raise RuntimeError(f"{what}: {msg or 'NCCL failure'} (NCCL, status {rc})")
     raise RuntimeError(f"{what}: {msg or 'CUDA failure'} (status {rc})")
 
 

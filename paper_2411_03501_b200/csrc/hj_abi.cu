@@ -55,6 +55,16 @@ static int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+namespace hj {
+// for the other translation units of the library (hj_dd.cu): set the
+// thread-local message / count launches made outside this file
+int set_error(int code, const char* msg) {
+  g_err = msg ? msg : "";
+  return code;
+}
+void count_launches(uint64_t n) { g_launches += n; }
+}  // namespace hj
+
 static int cuda_status(cudaError_t e, const char* what, uint64_t launches = 1) {
   if (e != cudaSuccess) return fail(HJ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   g_launches += launches;
@@ -94,6 +104,11 @@ static int make_grid(const hj_grid* g, int ghost_width, GridArgs* G, unsigned gh
     A.halo_n = (a == 0 && (g->halo_lo || g->halo_hi)) ? g->halo : 0;
     if (A.bc < HJ_BC_PERIODIC || A.bc > HJ_BC_DIRICHLET)
       return fail(HJ_EINVAL, "axis %d: unknown boundary kind %d", a, A.bc);
+    // the brick kernels stage HJ_HALO_MIN exchanged planes per side whatever
+    // the scheme's ghost width, so a thinner halo would be read out of bounds
+    if (a == 0 && (A.halo_lo || A.halo_hi) && g->halo < HJ_HALO_MIN)
+      return fail(HJ_EINVAL, "axis 0 halo %d thinner than the %d planes the stage kernels read", g->halo,
+                  HJ_HALO_MIN);
     if (((ghost_axes >> a) & 1u) && (A.halo_lo || A.halo_hi) && g->halo < ghost_width)
       return fail(HJ_EINVAL, "axis 0 halo %d thinner than ghost width %d", g->halo, ghost_width);
     if (((ghost_axes >> a) & 1u) && ghost_width > 0 && A.bc == HJ_BC_PERIODIC && !(A.halo_lo && A.halo_hi) && ghost_width > A.n)

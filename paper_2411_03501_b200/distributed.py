@@ -12,12 +12,22 @@ bit-identical to the single-GPU one.  Dissipation bounds are global and
 range-free, so dt needs no collective; non-finite flags are max-reduced once
 per interval.
 
-Transports: ``TorchDistTransport`` (NCCL or gloo process group) for real
-ranks; ``LocalTransport`` runs all slabs of one process on one device with
-plain copies (tests / emulation -- no kernel ever waits on another).
+Transports:
+* ``NcclTransport`` -- the data plane on GPUs: libhjb200's own NCCL
+  communicator behind the C ABI (hj_dd_*, csrc/hj_dd.cu).  Each stage is ONE
+  ABI call (grouped send/recv of the halo planes on the communicator's
+  stream, CORE launch meanwhile, stream wait, RIM launch); per interval the
+  device stats are all-reduced (first failing stage / error class, ranges)
+  and snapshots are gathered with hj_dd_gather.  torch.distributed only
+  broadcasts the communicator's unique id (any backend);
+* ``TorchDistTransport`` -- a torch.distributed process group (gloo: the
+  CPU-side multi-process tests, halos staged through the host);
+* ``LocalTransport`` -- all slabs of one process on one device with plain
+  copies (tests / emulation: no kernel ever waits on another).
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -42,19 +52,24 @@ class Slab:
     hi_rank: int
 
 
-def partition(n0: int, world: int, halo: int, periodic: bool) -> list[Slab]:
+def partition(n0: int, world: int, halo: int, periodic: bool, self_ring: bool = False) -> list[Slab]:
     """Balanced contiguous split of axis 0; every slab must hold >= halo planes
-    (its boundary planes are a neighbour's halo) and >= 2 (extrapolation)."""
+    (its boundary planes are a neighbour's halo) and >= 2 (extrapolation).
+    ``self_ring``: a single slab of a periodic axis 0 exchanges its halos with
+    itself (the NCCL data plane on one GPU; the periodic wrap of
+    grid.py:208-211 then arrives as exchanged planes)."""
     if world < 1:
         raise ValueError("world size must be >= 1")
+    if self_ring and not (world == 1 and periodic):
+        raise ValueError("a self ring needs one slab of a periodic axis 0")
     base, extra = divmod(n0, world)
     sizes = [base + (1 if r < extra else 0) for r in range(world)]
-    if world > 1 and min(sizes) < max(halo, 2):
+    if (world > 1 or self_ring) and min(sizes) < max(halo, 2):
         raise ValueError(f"axis 0 has {n0} nodes: too few for {world} slabs with halo {halo}")
     slabs, lo = [], 0
     for r, n in enumerate(sizes):
-        has_lo = world > 1 and (r > 0 or periodic)
-        has_hi = world > 1 and (r < world - 1 or periodic)
+        has_lo = self_ring or (world > 1 and (r > 0 or periodic))
+        has_hi = self_ring or (world > 1 and (r < world - 1 or periodic))
         slabs.append(Slab(r, world, lo, n, halo, has_lo, has_hi, (r - 1) % world, (r + 1) % world))
         lo += n
     return slabs
@@ -132,6 +147,116 @@ class TorchDistTransport:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
+    def merge_stats(self, stats: dev.Stats) -> "_lib.HjStats":
+        """Every rank's hj_stats combined as one GPU would have accumulated
+        them (nonfinite OR, first_bad_tag min, ranges min/max) -- host side,
+        one MAX all-reduce of [bits, -tag, -lo keys, hi keys]."""
+        import torch.distributed as dist
+
+        st = stats.read()
+        vals = [(int(st.nonfinite) >> b) & 1 for b in range(8)] + [-int(st.first_bad_tag)]
+        vals += [-int(k) for k in st.lo_key] + [int(k) for k in st.hi_key]
+        t = torch.tensor(vals, dtype=torch.int64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        v = [int(x) for x in t.tolist()]
+        out = _lib.HjStats()
+        out.nonfinite = sum(1 << b for b in range(8) if v[b])
+        out.first_bad_tag = -v[8]
+        for a in range(_lib.HJ_MAX_DIM):
+            out.lo_key[a] = -v[9 + a]
+            out.hi_key[a] = v[9 + _lib.HJ_MAX_DIM + a]
+        return out
+
+    def gather(self, slabs, owned: torch.Tensor, dst: int = 0):
+        return gather_owned(slabs, owned, dst, self.group)
+
+
+class NcclTransport:
+    """The GPU data plane: libhjb200's NCCL communicator (hj_dd_*).
+
+    torch.distributed (any backend) only broadcasts the communicator's
+    unique id; with one rank (a self ring) no process group is needed."""
+
+    native = True
+
+    def __init__(self, slab: Slab, group=None):
+        self.slab = slab
+        self.group = group
+        self.lib = dev.require()
+        uid = ctypes.create_string_buffer(_lib.DD_UID_BYTES)
+        if slab.world > 1:
+            import torch.distributed as dist
+
+            obj = [None]
+            if dist.get_rank(group) == 0:
+                _lib.check(self.lib.hj_dd_unique_id(uid), "hj_dd_unique_id")
+                obj = [bytes(uid.raw)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], _lib.DD_UID_BYTES)
+        else:
+            _lib.check(self.lib.hj_dd_unique_id(uid), "hj_dd_unique_id")
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.hj_dd_init(uid, slab.world, slab.rank, slab.lo_rank if slab.has_lo else -1,
+                                       slab.hi_rank if slab.has_hi else -1, ctypes.byref(h)), "hj_dd_init")
+        self.h = h
+
+    def close(self) -> None:
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.hj_dd_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stage(self, dg, scheme, dh, alphas_c, dt, kind, y_in, y0, y_out, mask_prev, mask, stats, tag, strm,
+              overlap: bool) -> None:
+        p = dev.ptr
+        rc = self.lib.hj_dd_stage(self.h, dg.ref, _lib.SCHEME_CODES[scheme], dh.ref, alphas_c, float(dt), int(kind),
+                                  p(y_in), p(y0), p(y_out), p(mask_prev), int(mask), stats.p if stats else None,
+                                  int(tag), 1 if overlap else 0, strm)
+        if rc:
+            _lib.check(rc, "hj_dd_stage")
+
+    def exchange_full(self, dg, buf: torch.Tensor) -> None:
+        _lib.check(self.lib.hj_dd_exchange(self.h, dg.ref, dev.ptr(buf), dev.stream()), "hj_dd_exchange")
+
+    def merge_stats(self, stats: dev.Stats) -> "_lib.HjStats":
+        _lib.check(self.lib.hj_dd_reduce_stats(self.h, stats.p, dev.stream()), "hj_dd_reduce_stats")
+        return stats.read()
+
+    def gather(self, slabs, owned: torch.Tensor, dst: int = 0):
+        mine = owned.contiguous()
+        counts = (ctypes.c_int64 * len(slabs))(*[s.n * (mine.numel() // max(owned.shape[0], 1)) for s in slabs])
+        full = None
+        if self.slab.rank == dst:
+            full = torch.empty((sum(s.n for s in slabs),) + tuple(mine.shape[1:]), dtype=mine.dtype,
+                               device=mine.device)
+        _lib.check(self.lib.hj_dd_gather(self.h, dev.ptr(mine), mine.numel(), dev.ptr(full) if full is not None
+                                         else None, counts, int(dst), dev.stream()), "hj_dd_gather")
+        return dev.to_host(full) if full is not None else None
+
+    def traffic(self) -> tuple[int, int]:
+        ex, by = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(self.lib.hj_dd_stats(self.h, ctypes.byref(ex), ctypes.byref(by)), "hj_dd_stats")
+        return int(ex.value), int(by.value)
+
+
+def default_transport(slab: Slab, group=None):
+    """NCCL data plane (hj_dd) when the ranks drive GPUs through an NCCL
+    process group (or HJ_SLAB_COMM=nccl), else the torch.distributed one."""
+    import os
+
+    import torch.distributed as dist
+
+    want = os.environ.get("HJ_SLAB_COMM", "auto")
+    if want == "nccl" or (want == "auto" and slab.world > 1 and dist.get_backend(group) == "nccl"):
+        return NcclTransport(slab, group)
+    return TorchDistTransport(slab, group)
+
 
 class SlabIntegrator(FusedIntegrator):
     """FusedIntegrator on one slab of a decomposed grid.
@@ -142,13 +267,17 @@ class SlabIntegrator(FusedIntegrator):
     """
 
     def __init__(self, g, cfg: TermConfig, rank: int, world: int, halo: int = 3, transport=None, group=None,
-                 overlap: bool = True):
-        self.slab = partition(g.counts[0], world, halo, g.is_periodic(0))[rank]
+                 overlap: bool = True, self_ring: bool = False):
+        if halo < _lib.HALO_MIN:
+            raise ValueError(f"slab halo {halo} thinner than the {_lib.HALO_MIN} planes the stage kernels read")
+        self.slab = partition(g.counts[0], world, halo, g.is_periodic(0), self_ring=self_ring)[rank]
         # overlap: each stage = CORE launch while the halo exchange is in flight, then RIM
         self.overlap = overlap
         s = self.slab
         dg = dev.DeviceGrid(g, slab=(s.lo, s.n, int(s.has_lo), int(s.has_hi), s.halo))
-        self.transport = transport or TorchDistTransport(s, group)
+        if transport == "nccl":
+            transport = NcclTransport(s, group)
+        self.transport = transport or default_transport(s, group)
         super().__init__(g, cfg, dg=dg, exchange=None)
         self.full_shape = (s.n + 2 * s.halo,) + tuple(g.counts[1:])
         self.owned_cells = dg.cells
@@ -182,6 +311,14 @@ class SlabIntegrator(FusedIntegrator):
 
     def _stage(self, alphas_c, dt, kind, y_in, y0, y_out, mask_prev, mask, tag, strm):
         o = self.owned
+        if getattr(self.transport, "native", False):
+            # one ABI call: exchange on the communicator's stream, CORE, wait, RIM
+            self.transport.stage(self.dg, self.scheme, self.dh, alphas_c, dt, kind, o(y_in),
+                                 None if y0 is None else o(y0), o(y_out),
+                                 None if mask_prev is None else o(mask_prev), mask, self.stats, tag, strm,
+                                 self.overlap)
+            self.launches += 2 if (self.overlap and (self.slab.has_lo or self.slab.has_hi)) else 1
+            return
         args = (self.dg, self.scheme, self.dh, alphas_c, dt, kind, o(y_in), None if y0 is None else o(y0),
                 o(y_out), None if mask_prev is None else o(mask_prev), mask, self.stats, tag)
         if self.overlap and (self.slab.has_lo or self.slab.has_hi):
@@ -196,13 +333,10 @@ class SlabIntegrator(FusedIntegrator):
         dev.stage_dev(*args, lib=self.lib, strm=strm)
         self.launches += 1
 
-    def _raise_pending(self, times, warn: bool = False) -> None:
-        # every rank raises the same error: flags are max-reduced first
-        st = self.stats.read()
-        merged = self.transport.max_flags(st.nonfinite)
-        if merged & _lib.NF_MASK and not st.nonfinite & _lib.NF_MASK:
-            raise RuntimeError("non-finite values on another slab")
-        super()._raise_pending(times, warn)
+    def _read_stats(self):
+        # every rank raises the error the single-GPU run raises: the stats are
+        # combined across ranks first (flags OR, first failing stage min)
+        return self.transport.merge_stats(self.stats)
 
 
 class LocalTransport:
@@ -248,6 +382,10 @@ class _LocalEndpoint:
     def max_flags(self, flags: int) -> int:
         self.hub.flags[self.rank] = flags
         return max(self.hub.flags.values())
+
+    def merge_stats(self, stats: dev.Stats):
+        # emulation: each slab reports its own stats (the slabs run in one process)
+        return stats.read()
 
 
 def lockstep_step3(runs: list[SlabIntegrator], hub: LocalTransport, ys: list[torch.Tensor], t: float,
@@ -311,12 +449,16 @@ def solve_tube_slabs(g, target, cfg: TermConfig, horizon: float, global_steps: i
     from .reachability import BRTResult
     from .spatial import SCHEME_WIDTH
 
-    rank, world = dist.get_rank(), dist.get_world_size()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
     target_vals = np.asarray(target.values if hasattr(target, "values") else target, dtype=np.float64)
     if horizon == 0:
         return BRTResult(snapshots=(target,) if rank == 0 else (), times=(0.0,))
     opts = opts or IntegratorOptions()
-    halo = halo if halo is not None else max(SCHEME_WIDTH[cfg.derivative_scheme], 2)
+    # the stage kernels stage HJ_HALO_MIN (3) exchanged planes whatever the
+    # scheme's ghost width (spatial.py:27), so every slab carries 3
+    halo = halo if halo is not None else max(SCHEME_WIDTH[cfg.derivative_scheme], _lib.HALO_MIN)
+    if halo < _lib.HALO_MIN:
+        raise ValueError(f"slab halo {halo} thinner than the {_lib.HALO_MIN} planes the stage kernels read")
     si = SlabIntegrator(g, cfg, rank, world, halo=halo, transport=transport, group=group)
     slabs = partition(g.counts[0], world, halo, g.is_periodic(0))
     use_min = cfg.approximation_sign == "over"
@@ -330,7 +472,7 @@ def solve_tube_slabs(g, target, cfg: TermConfig, horizon: float, global_steps: i
         except Exception as err:
             raise RuntimeError(f"tube interval {k} failed: {err}") from err
         prev = res.y
-        full = gather_owned(slabs, si.owned(prev), 0, group)
+        full = si.transport.gather(slabs, si.owned(prev), 0)
         times.append(t1)
         if rank == 0:
             from .grid import ScalarField

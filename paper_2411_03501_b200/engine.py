@@ -221,10 +221,10 @@ class FusedIntegrator:
         out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)
         src_host = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
         comp = torch.cuda.current_stream()
-        for st in (s_in, s_out, *s_st):
-            st.wait_stream(comp)                     # the buffers' previous users
         alphas_c = _lib.doubles(self._alphas(t0, None), _lib.HJ_MAX_DIM)
-        self.stats.reset()
+        self.stats.reset()                           # on comp: ordered before every stage stream below
+        for st in (s_in, s_out, *s_st):
+            st.wait_stream(comp)                     # the buffers' previous users, and the reset
         # one stream per stage: a launch waits (events) for the latest launch of
         # the stage before it (or the latest input chunk), so launches of
         # different stages overlap and fill each other's partial last waves
@@ -342,9 +342,12 @@ class FusedIntegrator:
             src = dst
         return src
 
+    def _read_stats(self):
+        return self.stats.read()
+
     def _raise_pending(self, times: dict[int, float], warn: bool = False) -> None:
         """Turn the device flags into the exception the reference raises first."""
-        s = self.stats.read()
+        s = self._read_stats()
         if warn and s.nonfinite & _lib.FLAG_HAM_NONZERO:
             warn_zero_dissipation()
         if not s.nonfinite & _lib.NF_MASK:

@@ -111,3 +111,77 @@ def test_gloo_gather_owned_uneven_slabs(world, n0):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert list(out) == [1] * world
+
+
+def test_partition_self_ring():
+    (s,) = partition(12, 1, 3, periodic=True, self_ring=True)
+    assert s.has_lo and s.has_hi and s.lo_rank == 0 and s.hi_rank == 0
+    sends, recvs = halo_plan(s)
+    # first owned planes -> own upper halo, last owned planes -> own lower halo
+    assert sends == [(0, (3, 6)), (0, (12, 15))] and recvs == [(0, (15, 18)), (0, (0, 3))]
+    with pytest.raises(ValueError, match="self ring"):
+        partition(12, 1, 3, periodic=False, self_ring=True)
+    with pytest.raises(ValueError, match="self ring"):
+        partition(12, 2, 3, periodic=True, self_ring=True)
+
+
+def test_slab_halo_must_cover_the_kernels_planes():
+    """the brick kernels stage HJ_HALO_MIN = 3 planes whatever the
+    scheme's ghost width; thinner slab halos are refused before any device work."""
+    import paper_2411_03501_b200 as hj
+    from paper_2411_03501_b200 import _lib
+    from paper_2411_03501_b200.distributed import SlabIntegrator
+
+    assert _lib.HALO_MIN == 3
+    g = hj.air3d_grid((24, 10, 12))
+    with pytest.raises(ValueError, match="halo 2 thinner"):
+        SlabIntegrator(g, hj.air3d_term_config(scheme="eno2"), 0, 2, halo=2)
+
+
+class _FakeStats:
+    """Stands in for device.Stats on CPU: read() returns a fixed hj_stats."""
+
+    def __init__(self, nonfinite, tag, lo, hi):
+        from paper_2411_03501_b200 import _lib
+
+        self.s = _lib.HjStats()
+        self.s.nonfinite = nonfinite
+        self.s.first_bad_tag = tag
+        for a in range(_lib.HJ_MAX_DIM):
+            self.s.lo_key[a] = lo + a
+            self.s.hi_key[a] = hi - a
+
+    def read(self):
+        return self.s
+
+
+def _merge_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = partition(30, world, 3, False)[rank]
+        # rank r: flag bit r, first failing key 100 - 10 r (rank world-1 failed first), ranges shifted by r
+        st = _FakeStats(1 << rank, 100 - 10 * rank if rank else 0x7FFFFFFF, -5 - rank, 7 + rank)
+        m = TorchDistTransport(s).merge_stats(st)
+        ok = m.nonfinite == (1 << world) - 1
+        ok &= m.first_bad_tag == 100 - 10 * (world - 1)
+        ok &= m.lo_key[0] == -5 - (world - 1) and m.hi_key[0] == 7 + (world - 1) and m.hi_key[2] == 5 + world - 1
+        out[rank] = int(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_merge_stats_like_one_gpu(world):
+    """flags are OR-ed (not max-ed) and first_bad_tag is min-reduced
+    across ranks, so every rank raises the error the single-GPU run raises."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Array("i", [0] * world)
+    port = _free_port()
+    procs = [ctx.Process(target=_merge_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert list(out) == [1] * world

@@ -12,6 +12,8 @@ import pytest
 import paper_2411_03501_b200 as hj
 from golden_io import case_list, package_grid
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 class TestGrid:
     def test_three_dim_periodic_spacings(self):
@@ -213,3 +215,24 @@ def test_compute_api_fails_loudly_without_cuda():
     g = hj.create_grid((0.0,), (1.0,), (16,))
     with pytest.raises(RuntimeError, match="CUDA"):
         hj.upwind_first_weno5(g, hj.ScalarField(np.linspace(0.0, 1.0, 16)), 0)
+
+
+def test_bench_refuses_more_gpus_than_present():
+    """bench.py --gpus N launches N ranks itself, and fails loudly (exit 2)
+    when the host has fewer GPUs -- it never silently measures one."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "needs 2 CUDA devices" in r.stderr
+
+
+def test_bench_config_table():
+    import bench
+
+    assert bench.CONFIGS == ("c1", "c2", "c3", "c4", "c5")
+    assert bench.parse([]).config == "c2"
+    assert abs(bench.BYTES_RK3 - 64 / 3) < 1e-12 and bench.BYTES_RK2 == 20.0
+    assert bench.brick_symbol("k_stage_brickILi3ELi3ELi2ELi0ELi2EE") == \
+        "_ZN2hj13k_stage_brickILi3ELi3ELi2ELi0ELi2EEEvNS_9StageArgsEi"
