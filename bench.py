@@ -59,7 +59,7 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=CONFIGS)
-    ap.add_argument("--n", type=int, default=None, help="override the nodes per axis of the config (tests)")
+    ap.add_argument("--size", dest="n", type=int, default=None, help="override the nodes per axis of the config (tests)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tolerance-mode", action="store_true", help="skip the weno5_fma side measurement")
@@ -111,6 +111,11 @@ class ClockSampler:
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes ~0.1-0.3 s to start: the timed region begins once it samples
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.n_before = len(self.lines)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -121,6 +126,10 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # a timed region shorter than the 20 ms period still gets the sample that follows it
+            t0 = time.perf_counter()
+            while len(self.lines) <= self.n_before and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -131,7 +140,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[max(0, getattr(self, "n_before", 1) - 1):]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue

@@ -262,6 +262,14 @@ int hj_mask(int64_t count, const double* prev, double* v, int mask, void* stream
 /* reachability.py:257-260: *d_count += #{v < level} */
 int hj_count_below(int64_t count, const double* v, double level,
                    unsigned long long* d_count, void* stream);
+/* Tube acceptance checks on the device (test_reachability.py:218-285 over the
+ * mask of reachability.py:249), no field leaves the GPU.  Adds to d_out[4]:
+ *   [0] nesting violations   #{v > prev} (HJ_MASK_MIN) / #{v < prev} (HJ_MASK_MAX)
+ *   [1] containment violations #{v > target} / #{v < target}
+ *   [2] #{v < level}           (sublevel_volume's count, reachability.py:257-260)
+ *   [3] #{prev >= level and v < level}  (nodes captured during the interval) */
+int hj_tube_check(int64_t count, const double* prev, const double* v, const double* target, int mask, double level,
+                  unsigned long long* d_out, void* stream);
 /* Self-check of the hoisted-reciprocal division used by the fast kernels:
  * n random/special operand pairs, *d_mismatch += #{div_by(a,b) != a/b} (bitwise). */
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);

@@ -107,6 +107,7 @@ _SIGNATURES = [
     ("hj_integrate", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_int, c_double, c_double,
                              c_double, c_double, c_int, c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                              c_int, c_void_p, POINTER(c_double), POINTER(c_void_p), c_void_p]),
+    ("hj_tube_check", c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int, c_double, c_void_p, c_void_p]),
     ("hj_check_division", c_int, [c_int64, c_uint64, c_void_p, c_void_p]),
     ("hj_fp64_probe", c_int, [c_int, c_int, c_void_p, c_void_p]),
     ("hj_set_stage_kernel", c_int, [c_int]),

@@ -24,6 +24,8 @@ cudaError_t launch_mask(long long n, const double* prev, double* v, int mask, cu
 cudaError_t launch_count_below(long long n, const double* v, double level, unsigned long long* c,
                                cudaStream_t s);
 cudaError_t launch_stats_reset(hj_stats* st, cudaStream_t s);
+cudaError_t launch_tube_check(long long n, const double* prev, const double* v, const double* target, int mask_min,
+                              double level, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_costates(const GridArgs& G, const double* const* l, const double* const* r,
                             double* const* p, hj_stats* st, cudaStream_t s);
 cudaError_t launch_glf_delta(const GridArgs& G, const double* ahalf, const double* const* l,
@@ -464,6 +466,15 @@ int hj_count_below(int64_t count, const double* v, double level, unsigned long l
   if (!v || !d_count) return fail(HJ_EINVAL, "NULL pointer");
   if (count <= 0) return HJ_OK;
   return cuda_status(launch_count_below(count, v, level, d_count, (cudaStream_t)stream), "hj_count_below");
+}
+
+int hj_tube_check(int64_t count, const double* prev, const double* v, const double* target, int mask, double level,
+                  unsigned long long* d_out, void* stream) {
+  if (mask != HJ_MASK_MIN && mask != HJ_MASK_MAX) return fail(HJ_EINVAL, "unknown mask %d", mask);
+  if (!prev || !v || !target || !d_out) return fail(HJ_EINVAL, "NULL pointer");
+  if (count <= 0) return HJ_OK;
+  return cuda_status(launch_tube_check(count, prev, v, target, mask == HJ_MASK_MIN, level, d_out,
+                                       (cudaStream_t)stream), "hj_tube_check");
 }
 
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream) {

@@ -140,6 +140,39 @@ __global__ void k_count_below(long long n, const double* __restrict__ v, double 
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// Tube acceptance checks on the device (reference: test_reachability.py:218-285
+// over the mask of reachability.py:249), so a solve can verify its own tube
+// without copying fields to the host.  out[0] nesting violations (v above
+// prev for the min mask / below for the max mask), out[1] target-containment
+// violations (v above / below the target), out[2] #{v < level}, out[3]
+// #{prev >= level and v < level} (nodes captured during the interval).
+__global__ void k_tube_check(long long n, const double* __restrict__ prev, const double* __restrict__ v,
+                             const double* __restrict__ target, int mask_min, double level,
+                             unsigned long long* __restrict__ out) {
+  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = prev[i], b = v[i], g = target[i];
+    c0 += (mask_min ? (b > a) : (b < a)) ? 1ull : 0ull;
+    c1 += (mask_min ? (b > g) : (b < g)) ? 1ull : 0ull;
+    c2 += (b < level) ? 1ull : 0ull;
+    c3 += (!(a < level) && b < level) ? 1ull : 0ull;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+    c3 += __shfl_xor_sync(0xffffffffu, c3, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (c0) atomicAdd(&out[0], c0);
+    if (c1) atomicAdd(&out[1], c1);
+    if (c2) atomicAdd(&out[2], c2);
+    if (c3) atomicAdd(&out[3], c3);
+  }
+}
+
 __global__ void k_stats_reset(hj_stats* st) {
   const int t = threadIdx.x;
   if (t < HJ_MAX_DIM) {
@@ -251,6 +284,15 @@ cudaError_t launch_count_below(long long n, const double* v, double level, unsig
   if (b > 148 * 16) b = 148 * 16;
   if (b < 1) b = 1;
   k_count_below<<<(unsigned)b, 256, 0, s>>>(n, v, level, c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tube_check(long long n, const double* prev, const double* v, const double* target, int mask_min,
+                              double level, unsigned long long* out, cudaStream_t s) {
+  long long b = nblocks(n, 256);
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  k_tube_check<<<(unsigned)b, 256, 0, s>>>(n, prev, v, target, mask_min, level, out);
   return cudaGetLastError();
 }
 

@@ -251,6 +251,15 @@ def count_below_dev(v: torch.Tensor, level: float) -> int:
     return int(c.item())
 
 
+def tube_check_dev(prev: torch.Tensor, v: torch.Tensor, target: torch.Tensor, use_min: bool, level: float,
+                   out: torch.Tensor) -> None:
+    """hj_tube_check: add this interval's nesting / containment violations,
+    sublevel count and newly captured nodes to the int64[4] device tensor ``out``."""
+    lib = require()
+    check(lib.hj_tube_check(v.numel(), ptr(prev), ptr(v), ptr(target), _lib.MASK_MIN if use_min else _lib.MASK_MAX,
+                            float(level), out.data_ptr(), stream()), "hj_tube_check")
+
+
 def costates_dev(dg: DeviceGrid, Ls, Rs, stats: Stats | None):
     lib = require()
     P = [torch.empty_like(x) for x in Ls]

@@ -220,6 +220,13 @@ class FusedIntegrator:
         y_dev = bufs[0]
         out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)
         src_host = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
+        staged = None
+        if not src_host.is_pinned():
+            # a pageable input (a plain NumPy array, as a reference caller
+            # passes it): host threads copy it chunk by chunk into pinned
+            # staging memory, ahead of the DMA of the chunks before
+            staged = self._stage_pageable(src_host)
+            src_host = self._staging
         comp = torch.cuda.current_stream()
         alphas_c = _lib.doubles(self._alphas(t0, None), _lib.HJ_MAX_DIM)
         self.stats.reset()                           # on comp: ordered before every stage stream below
@@ -232,6 +239,9 @@ class FusedIntegrator:
         for op, k, lo, hi in pipeline_plan(n0, len(kinds), int(self.pipeline_chunk),
                                           first=int(self.pipeline_first), drain=int(self.pipeline_drain)):
             if op == "h2d":
+                if staged is not None:
+                    for f in staged.pop(lo):
+                        f.result()
                 with torch.cuda.stream(s_in):
                     y_dev[lo:hi].copy_(src_host[lo:hi], non_blocking=True)
                     last_ev[0] = torch.cuda.Event()
@@ -254,6 +264,31 @@ class FusedIntegrator:
         for st in (s_in, s_out, *s_st):
             comp.wait_stream(st)
         return out_host.numpy()
+
+    staging_threads = 8          # host threads copying a pageable input into pinned memory
+
+    def _stage_pageable(self, src: torch.Tensor) -> dict:
+        """Queue the copies of ``src`` into the cached pinned staging buffer in
+        the pipeline's H2D chunk order, split across host threads (NumPy copies
+        release the GIL).  Returns {chunk start plane: [futures]}."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        if getattr(self, "_staging", None) is None or self._staging.shape != src.shape:
+            self._staging = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        if getattr(self, "_stage_pool", None) is None:
+            self._stage_pool = ThreadPoolExecutor(max_workers=int(self.staging_threads),
+                                                  thread_name_prefix="hj-stage")
+        dst, srcn = self._staging.numpy(), src.numpy()
+        n0 = src.shape[0]
+        out: dict[int, list] = {}
+        for op, _, lo, hi in pipeline_plan(n0, 1, int(self.pipeline_chunk), first=int(self.pipeline_first),
+                                          drain=int(self.pipeline_drain)):
+            if op != "h2d":
+                continue
+            step = max(1, -(-(hi - lo) // int(self.staging_threads)))
+            out[lo] = [self._stage_pool.submit(np.copyto, dst[a:min(a + step, hi)], srcn[a:min(a + step, hi)])
+                       for a in range(lo, hi, step)]
+        return out
 
     # ------------------------------------------------------------ native loop
     def _native_ok(self, opts) -> bool:

@@ -235,15 +235,26 @@ class SnapshotPipe:
 
 def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
                opts: IntegratorOptions | None = None,
-               progress: Callable[[int, float, ScalarField], None] | None = None) -> BRTResult:
+               progress: Callable[[int, float, ScalarField], None] | None = None,
+               diagnostics: list | None = None, keep_snapshots: bool = True) -> BRTResult:
     """The tube driver of solve_brt for any dimension and RK order.
 
     ReachProblem insists on the 3-D rockets layout and solve_brt hard-wires
     RK3 (reachability.py:198-199, 246); this is the same loop with those two
     choices opened up (Air3D C1 runs RK2, the 4-D pair runs on 4 axes).
+
+    ``diagnostics`` (a list, registered device Hamiltonians): the tube's
+    acceptance checks (test_reachability.py:218-285) evaluated on the GPU per
+    interval (hj_tube_check) and appended as dicts -- nesting and target
+    containment violations, sublevel count and volume, nodes captured in the
+    interval -- with no field copied to the host for them.
+    ``keep_snapshots=False`` skips the per-interval snapshot copies: the
+    result then holds the target and the final field only (times likewise).
     """
     if horizon == 0:
         return BRTResult(snapshots=(target,), times=(0.0,))
+    if not keep_snapshots and (progress is not None or not cfg.on_device):
+        raise ValueError("keep_snapshots=False needs a registered device Hamiltonian and no progress callback")
     opts = opts or IntegratorOptions()
     use_min = cfg.approximation_sign == "over"
     snaps = [target]
@@ -253,6 +264,9 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
 
         fi = FusedIntegrator(g, cfg)
         prev = dev.to_dev(target.values)
+        target_dev = prev
+        counters = (torch.zeros((global_steps, 4), dtype=torch.int64, device=prev.device)
+                    if diagnostics is not None else None)
 
         def deliver(k, t, values):
             v = ScalarField._from_device(values)   # finiteness checked on the device
@@ -271,14 +285,26 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
                 except Exception as err:
                     pipe.drain()   # callbacks of the intervals that did finish
                     raise RuntimeError(f"tube interval {k} failed: {err}") from err
+                if counters is not None:
+                    dev.tube_check_dev(prev, res.y, target_dev, use_min, 0.0, counters[k - 1])
                 prev = res.y
                 # interval k's snapshot streams to the host while interval k+1
                 # computes; interval k-1's is handed out meanwhile
-                pipe.push(k, t1, prev)
+                if keep_snapshots:
+                    pipe.push(k, t1, prev)
                 t0 = t1
             pipe.drain()
         finally:
             pipe.close()
+        if counters is not None:
+            cell = float(np.prod(g.spacings))
+            for k, row in enumerate(counters.cpu().tolist(), start=1):
+                diagnostics.append({"interval": k, "t": horizon * k / global_steps, "nesting_violations": row[0],
+                                    "containment_violations": row[1], "sublevel_nodes": row[2],
+                                    "volume": cell * row[2], "captured": row[3]})
+        if not keep_snapshots:
+            final = ScalarField._from_device(dev.to_host(prev))
+            return BRTResult(snapshots=(target, final), times=(0.0, float(t0)))
         return BRTResult(snapshots=tuple(snaps), times=tuple(times))
 
     from .integrator import ode_cfl_1, ode_cfl_2
@@ -303,6 +329,32 @@ def solve_tube(g: Grid, target: ScalarField, cfg: TermConfig, horizon: float, gl
     return BRTResult(snapshots=tuple(snaps), times=tuple(times))
 
 
+_BATCH: "weakref.WeakKeyDictionary" = None
+
+
+def _batch_runner(g: Grid, cfg: TermConfig, batch: int):
+    """(FusedIntegrator over the stacked batch, pinned staging, copy pool) of
+    (grid, cfg, batch, device), reused across solve_tube_batch calls."""
+    global _BATCH
+    import weakref
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .engine import FusedIntegrator
+
+    if _BATCH is None:
+        _BATCH = weakref.WeakKeyDictionary()
+    per = _BATCH.setdefault(g, {})
+    key = (id(cfg), batch, torch.cuda.current_device())
+    hit = per.get(key)
+    if hit is None or hit[0] is not cfg:
+        fi = FusedIntegrator(g, cfg, dg=dev.DeviceGrid(g, batch=batch))
+        staging = torch.empty((batch,) + tuple(g.counts), dtype=dev.F64, pin_memory=True)
+        hit = (cfg, fi, staging, ThreadPoolExecutor(max_workers=8, thread_name_prefix="hj-batch"))
+        per.clear()   # one batch shape per grid is kept
+        per[key] = hit
+    return hit[1], hit[2], hit[3]
+
+
 def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
                      opts: IntegratorOptions | None = None, keep_snapshots: bool = True):
     """A batch of independent tubes sharing grid and dynamics (BASELINE C5:
@@ -313,17 +365,22 @@ def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_s
     times)."""
     if not cfg.on_device:
         raise TypeError("solve_tube_batch needs a registered device Hamiltonian")
-    from .engine import FusedIntegrator
-
-    tgt = np.stack([np.asarray(t.values if isinstance(t, ScalarField) else t, dtype=np.float64) for t in targets])
-    if tgt.shape[1:] != tuple(g.counts):
-        raise ValueError(f"targets have shape {tgt.shape[1:]}, grid needs {g.counts}")
-    if not np.isfinite(tgt).all():
-        raise ValueError("field contains non-finite values")
+    arrs = [np.asarray(t.values if isinstance(t, ScalarField) else t, dtype=np.float64) for t in targets]
+    for a in arrs:
+        if a.shape != tuple(g.counts):
+            raise ValueError(f"targets have shape {a.shape}, grid needs {g.counts}")
     opts = opts or IntegratorOptions()
-    dg = dev.DeviceGrid(g, batch=tgt.shape[0])
-    fi = FusedIntegrator(g, cfg, dg=dg)
-    prev = dev.to_dev(tgt)
+    fi, staging, pool = _batch_runner(g, cfg, len(arrs))
+    # the targets go to pinned staging on host threads (NumPy copies release
+    # the GIL), then one DMA; finiteness is checked on the device
+    st = staging.numpy()
+    for f in [pool.submit(np.copyto, st[b], a) for b, a in enumerate(arrs)]:
+        f.result()
+    prev = torch.empty(staging.shape, dtype=dev.F64, device=dev.device())
+    prev.copy_(staging, non_blocking=True)
+    if not bool(torch.isfinite(prev).all()):
+        raise ValueError("field contains non-finite values")
+    tgt = st.copy() if keep_snapshots else None
     snaps = [tgt] if keep_snapshots else []
     times = [0.0]
     use_min = cfg.approximation_sign == "over"
