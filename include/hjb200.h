@@ -275,8 +275,10 @@ int hj_tube_check(int64_t count, const double* prev, const double* v, const doub
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);
 /* Stage-kernel family (A/B measurements and test coverage): 0 per-node generic
  * kernel, 1 brick kernels when the grid has enough bricks (default), 2 brick
- * WENO5 kernel at 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid; -1 reads
- * HJ_STAGE_KERNEL from the environment.  Returns the previous setting. */
+ * WENO5 kernel at 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid, 4 WENO5
+ * walks rolled, 5 timing bound only (WENO5 bricks after a CTA's first skip
+ * their global->shared loads: WRONG results); -1 reads HJ_STAGE_KERNEL from
+ * the environment.  Returns the previous setting. */
 int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
  * iters x 8 independent DFMA chains (time it with events on `stream`). */

@@ -1,8 +1,9 @@
 // hj_abi.cu -- extern "C" entry points of libhjb200.so (declared in
 // include/hjb200.h).  Validation mirrors the reference's ValueError checks;
 // failures return HJ_E* and leave a thread-local message.
+#include <algorithm>
 #include <atomic>
-#include <map>
+#include <vector>
 #include <mutex>
 #include <cstdarg>
 #include <cstdio>
@@ -162,26 +163,55 @@ static int check_ham(const hj_ham* ham, int dim) {
 }
 
 // Device scratch for the 4-D pre-pass, cached per (device, stream) so that
-// solvers on different streams never share it; grown on demand (cudaFree
-// synchronises, so a buffer is never released while in use).
+// solvers on different streams never share it; grown on demand.  At most
+// SCRATCH_ENTRIES buffers live at once: the least recently used one is freed
+// (cudaFree synchronises the device, so a buffer is never released while a
+// kernel still uses it).
+constexpr size_t SCRATCH_ENTRIES = 4;
 static double* scratch_for(cudaStream_t s, size_t n_doubles) {
+  struct Entry {
+    int dev;
+    cudaStream_t stream;
+    double* p;
+    size_t n;
+    uint64_t used;
+  };
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, std::pair<double*, size_t>> cache;
+  static std::vector<Entry> cache;
+  static uint64_t clock = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  auto& e = cache[{dev, s}];
-  if (e.second < n_doubles) {
-    if (e.first) cudaFree(e.first);
-    e = {nullptr, 0};
-    double* p = nullptr;
-    if (cudaMalloc((void**)&p, n_doubles * sizeof(double)) != cudaSuccess) {
+  Entry* e = nullptr;
+  for (auto& c : cache)
+    if (c.dev == dev && c.stream == s) e = &c;
+  if (!e) {
+    if (cache.size() >= SCRATCH_ENTRIES) {
+      auto lru = std::min_element(cache.begin(), cache.end(),
+                                  [](const Entry& a, const Entry& b) { return a.used < b.used; });
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(lru->dev);
+      cudaFree(lru->p);
+      cudaSetDevice(cur);
+      cache.erase(lru);
+    }
+    cache.push_back(Entry{dev, s, nullptr, 0, 0});
+    e = &cache.back();
+  }
+  e->used = ++clock;
+  if (e->n < n_doubles) {
+    if (e->p) cudaFree(e->p);
+    e->p = nullptr;
+    e->n = 0;
+    if (cudaMalloc((void**)&e->p, n_doubles * sizeof(double)) != cudaSuccess) {
       cudaGetLastError();
+      e->p = nullptr;
       return nullptr;   // the caller falls back to the generic kernel
     }
-    e = {p, n_doubles};
+    e->n = n_doubles;
   }
-  return e.first;
+  return e->p;
 }
 
 // Derived constants computed once on the host side of the ABI.
@@ -326,8 +356,7 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
     const size_t span = (size_t)(P.g.batch_stride * (P.g.batch - 1) + P.g.cells);
     double* scratch = scratch_for(s, 2 * span);
     if (scratch) {
-      P.aux_p0 = scratch;
-      P.aux_d0 = scratch + span;
+      P.aux0 = scratch;   // span (p_avg0, d0) pairs
     }
   }
   bool handled = false;

@@ -55,6 +55,12 @@ struct BrickSmem {
   // ham_eval inputs of the brick: node coordinates along its three axes
   // [BZ | BYX | BYX], then the Hamiltonian's two tables along its third axis
   double crd[BZ + 4 * BYX];
+  // y0 of the combination stages for the fused first-axis walk: a two-node
+  // ring per thread, filled by cp.async two nodes ahead (slot (i & 1) holds
+  // node i).  Register slots filled by plain loads stalled ~8 % of the
+  // kernel's samples: the consuming move waited on the scoreboard of the
+  // youngest refill load, issued just before it (ncu source page, r01).
+  double qy[2 * BRICK_THREADS];
 };
 constexpr int CRD_Y = BZ, CRD_X = BZ + BYX, CRD_T0 = BZ + 2 * BYX, CRD_T1 = BZ + 3 * BYX;
 
@@ -62,20 +68,24 @@ constexpr int CRD_Y = BZ, CRD_X = BZ + BYX, CRD_T0 = BZ + 2 * BYX, CRD_T1 = BZ +
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
-// UNR: unroll of the WENO walk (the window rotates with period 4)
+// UNR: unroll of the WENO walk (the window rotates with period 4).  The walk
+// covers the brick edge N but stops after the first nv nodes (nv < N on the
+// partial bricks of the far faces: 121 = 7*16 + 9 nodes, the 4-D grid of
+// C4, leaves 7 of the last brick's 16 nodes outside the domain -- their
+// steps would only occupy the FP64 pipe).  The bound is warp-uniform: lanes
+// of a walk warp share the walk axis' brick extent.
 template <int SCHEME, int UNR, int N, class Load, class Emit>
-__device__ __forceinline__ void line_walk(const Load& ld, const Spacing& sp, const Emit& emit) {
-  constexpr int n = N;
+__device__ __forceinline__ void line_walk(const Load& ld, const Spacing& sp, const Emit& emit, int nv) {
   if constexpr (SCHEME == HJ_WENO5) {
-    weno5_line<UNR, N>(ld, n, weno_divisors(sp.h), emit);
+    weno5_line<UNR, N>(ld, nv, weno_divisors(sp.h), emit);
   } else if constexpr (SCHEME == HJ_WENO5_FMA) {
-    weno5_fma_line<UNR, N>(ld, n, sp.rh, emit);
+    weno5_fma_line<UNR, N>(ld, nv, sp.rh, emit);
   } else if constexpr (SCHEME == HJ_ENO3) {
-    eno3_line(ld, n, eno_divisors(sp), emit);
+    eno3_line(ld, min(nv, N), eno_divisors(sp), emit);
   } else if constexpr (SCHEME == HJ_ENO2) {
-    eno2_line(ld, n, eno_divisors(sp), emit);
+    eno2_line(ld, min(nv, N), eno_divisors(sp), emit);
   } else {
-    first_line(ld, n, eno_divisors(sp), emit);
+    first_line(ld, min(nv, N), eno_divisors(sp), emit);
   }
 }
 
@@ -124,11 +134,16 @@ __device__ __forceinline__ BrickCoord brick_coord(const BrickView<AO>& V, int li
   return c;
 }
 
-// L2 prefetch of a brick's rows, issued while the current brick computes
+// L2 prefetch of a brick's rows, issued while the current brick computes:
+// the stage input with its halos, and the per-node inputs of the fused
+// first-axis walk (y0 of the combination stages, the tube mask's previous
+// snapshot, the 4-D pre-pass scratch), which would otherwise be HBM misses
+// inside the walk
 template <int AO>
-__device__ __forceinline__ void prefetch_brick(const GridArgs& G, const BrickView<AO>& V, const double* vin0,
+__device__ __forceinline__ void prefetch_brick(const StageArgs& P, const GridArgs& G, const BrickView<AO>& V,
                                                const BrickCoord& c, int t) {
-  const double* vb = vin0 + V.slice_base(G, c.b);
+  const long long sb = V.slice_base(G, c.b);
+  const double* vb = P.y_in + sb;
   for (int r = t; r < (BZ + 2 * HB) * SVR; r += BRICK_THREADS) {
     const int z = r / SVR - HB, yy = r % SVR - HB;
     const int gz = c.z0 + z, gy = c.y0 + yy;
@@ -137,6 +152,26 @@ __device__ __forceinline__ void prefetch_brick(const GridArgs& G, const BrickVie
     const double* p = vb + gz * V.s0 + gy * V.s1 + gx;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
+  }
+  // per-node streams of the fused walk: one brick row (16 nodes) per thread and stream
+  const int z = t / BYX, yy = t % BYX;   // BZ x BYX = 128 rows per stream
+  const int gz = c.z0 + (z & (BZ - 1)), gy = c.y0 + yy;
+  if (gz >= V.n0 || gy >= V.n1) return;
+  const long long off = sb + (long long)gz * V.s0 + (long long)gy * V.s1 + c.x0;
+  if (z < BZ) {   // threads 0-127: y0, then the 4-D pairs; 128-255: the mask's previous snapshot
+    if (P.stage >= HJ_STAGE_RK2_AVG && P.y0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(P.y0 + off));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(P.y0 + off + 15));
+    }
+    if (AO && P.aux0) {   // 16 (p_avg0, d0) pairs = 256 B
+      const double* p = P.aux0 + 2 * off;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 31));
+    }
+  } else if (P.mask != HJ_MASK_NONE && P.mask_prev) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(P.mask_prev + off));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(P.mask_prev + off + 15));
   }
 }
 
@@ -152,7 +187,8 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
-                                            const BrickCoord c, unsigned& flags, const BrickCoord* next);
+                                            const BrickCoord c, unsigned& flags, const BrickCoord* next,
+                                            bool load);
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const StageArgs P, int nbricks) {
@@ -167,7 +203,8 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
     const int nxt = lin + gridDim.x;
     BrickCoord cn;
     if (nxt < nbricks) cn = brick_coord(V, nxt);
-    stage_brick<SCHEME, HAM, MINB, AO, UNR>(P, V, S, c, flags, nxt < nbricks ? &cn : nullptr);
+    stage_brick<SCHEME, HAM, MINB, AO, UNR>(P, V, S, c, flags, nxt < nbricks ? &cn : nullptr,
+                                            !P.skip_loads || lin == (int)blockIdx.x);
     __syncthreads();   // shared memory is reused by the next brick
   }
   if (P.stats) {
@@ -178,7 +215,8 @@ __global__ void __launch_bounds__(BRICK_THREADS, MINB) k_stage_brick(const Stage
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
-                                            const BrickCoord c, unsigned& flags, const BrickCoord* next) {
+                                            const BrickCoord c, unsigned& flags, const BrickCoord* next,
+                                            bool load) {
   constexpr int WALK_UNROLL = UNR;   // WENO walk unroll (removes window rotation moves)
   const GridArgs& G = P.g;
   const AxisView& A0 = G.ax[AO];
@@ -200,7 +238,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // (8 B, no register staging, all in flight at once); on boundary bricks the
   // extrapolated / dirichlet ghosts are then synthesised from the landed edge
   // nodes (no synchronous global loads on the load path).
-  {
+  if (load) {
     static_assert(BZ == BRICK_THREADS / 32, "one warp per brick plane");
     const int lane = t & 31, warp = t >> 5;
     const int z = warp, gz = z0 + z;
@@ -273,29 +311,37 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       const bool syn_zp = gz >= n0 && jz == GI_SYNTH;                       // this warp's plane
       const bool syn_zh = ghost_index(A0, z0 - 1) == GI_SYNTH || ghost_index(A0, z0 + BZ) == GI_SYNTH ||
                           ghost_index(A0, z0 + BZ + HB - 1) == GI_SYNTH;
-      srow = &S.v[z * PLANE + lane];
-      for (int yy = 0; yy < SVR && (syn_y || syn_x || syn_zp); ++yy, srow += SVP) {
-        const bool yin = yy >= HB && yy < HB + BYX;
-        if (!lane_on || !(yin || xin)) continue;
-        const int gy = y0 + yy - HB;
-        const bool gy_in = gy >= 0 && gy < n1;
-        if (gz < n0) {
-          if (!gy_in && !gx_in) continue;
-          if (!gy_in && ghost_index(A1, gy) == GI_SYNTH) {          // second-axis ghost
-            const int ye = (gy < 0 ? 0 : n1 - 1) - y0 + HB, yi = (gy < 0 ? 1 : n1 - 2) - y0 + HB;
-            *srow = ghost_synth(A1, gy, S.v[z * PLANE + ye * SVP + lane], S.v[z * PLANE + yi * SVP + lane]);
-          } else if (!gx_in && jx == GI_SYNTH) {                     // third-axis ghost
-            const int xe = (gx < 0 ? 0 : n2 - 1) - x0 + HB, xi = (gx < 0 ? 1 : n2 - 2) - x0 + HB;
-            *srow = ghost_synth(A2, gx, S.v[z * PLANE + yy * SVP + xe], S.v[z * PLANE + yy * SVP + xi]);
+      // Only the ghost slots some walk reads are visited: a second-axis ghost
+      // row at the brick's in-domain columns, a third-axis ghost column at its
+      // in-domain rows, a first-axis ghost plane at its in-domain (y, x); each
+      // reads only in-domain slots that phase 1 loaded (never another ghost).
+      if (gz < n0 && lane_on) {
+        double* colp = &S.v[z * PLANE + lane];
+        if (syn_y && xin && gx_in) {
+          const int lo_end = min(SVR, HB - y0);        // rows with gy < 0
+          const int hi_beg = max(0, n1 - y0 + HB);     // rows with gy >= n1
+          if (lo_end > 0) {
+            const double e = colp[(HB - y0) * SVP], in = colp[(HB - y0 + 1) * SVP];
+            for (int yy = 0; yy < lo_end; ++yy) colp[yy * SVP] = ghost_synth(A1, y0 + yy - HB, e, in);
           }
-        } else if (gy_in && gx_in && jz == GI_SYNTH) {                 // first-axis ghost
-          const int re = n0 - 1 - z0, ri = n0 - 2 - z0;   // re in [0, BZ), ri >= -1
-          const double edge = S.v[re * PLANE + yy * SVP + lane];
-          double inner;
-          if (ri >= 0) inner = S.v[ri * PLANE + yy * SVP + lane];
-          else if (yin && xin) inner = pz(ri, yy - HB, lane - HB);
-          else inner = vin[(long long)(n0 - 2) * s0 + gy * s1 + gx];
-          *srow = ghost_synth(A0, gz, edge, inner);
+          if (hi_beg < SVR) {
+            const double e = colp[(n1 - 1 - y0 + HB) * SVP], in = colp[(n1 - 2 - y0 + HB) * SVP];
+            for (int yy = hi_beg; yy < SVR; ++yy) colp[yy * SVP] = ghost_synth(A1, y0 + yy - HB, e, in);
+          }
+        }
+        if (syn_x && !gx_in) {                          // this lane is a third-axis ghost column
+          const int xe = (gx < 0 ? 0 : n2 - 1) - x0 + HB, xi = (gx < 0 ? 1 : n2 - 2) - x0 + HB;
+          const int rows = min(BYX, n1 - y0);
+          double* row = &S.v[z * PLANE + HB * SVP];
+          for (int yy = 0; yy < rows; ++yy, row += SVP) row[lane] = ghost_synth(A2, gx, row[xe], row[xi]);
+        }
+      } else if (syn_zp && xin && gx_in) {              // this warp's plane lies beyond the last one
+        const int re = n0 - 1 - z0, ri = n0 - 2 - z0;   // re in [0, BZ), ri >= -1
+        const int rows = min(BYX, n1 - y0);
+        for (int y = 0; y < rows; ++y) {
+          const double edge = S.v[re * PLANE + (y + HB) * SVP + lane];
+          const double inner = ri >= 0 ? S.v[ri * PLANE + (y + HB) * SVP + lane] : pz(ri, y, lane - HB);
+          S.v[z * PLANE + (y + HB) * SVP + lane] = ghost_synth(A0, gz, edge, inner);
         }
       }
 #pragma unroll
@@ -339,25 +385,25 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
     S.crd[t] = val;
   }
   __syncthreads();
-  if (next) prefetch_brick<AO>(G, V, P.y_in, *next, t);
+  if (next) prefetch_brick<AO>(P, G, V, *next, t);
 
-  // the first-axis walk's y0 inputs (RK2/RK3 combination stages) are read two
-  // nodes ahead; the first two are issued here so that their latency hides
-  // behind the second/third-axis walks
-  // (3-D only: the 4-D kernel has no registers to spare across the walks, it
-  // reads them one node ahead inside the first-axis walk)
-  constexpr int QD = AO ? 1 : (SCHEME == HJ_WENO5_FMA ? 4 : 2);   // exact: more would spill
+  // the first-axis walk's y0 inputs (RK2/RK3 combination stages) go through
+  // the per-thread shared ring S.qy, two nodes ahead; the first two copies are
+  // issued here so that their latency hides behind the second/third-axis
+  // walks.  One cp.async group per node: at node i, wait_group 1 completes
+  // exactly node i's copy (node i+1's may stay in flight).
   const int cy = t / BYX, cx = t % BYX;
   const bool col_on = y0 + cy < n1 && x0 + cx < n2;
   const long long coff0 = (long long)z0 * s0 + (long long)(y0 + cy) * s1 + (x0 + cx);
   const double* __restrict__ y0p = P.y0 ? P.y0 + base : nullptr;
   const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
   const int zmax = n0 - z0;   // nodes of this column inside the domain (may exceed BZ)
-  double qy[QD];
-  if constexpr (AO == 0) {
+  if (need_y0) {
 #pragma unroll
-    for (int k = 0; k < QD; ++k)
-      qy[k] = (col_on && need_y0 && k < zmax && k < BZ) ? y0p[coff0 + (long long)k * s0] : 0.0;
+    for (int k = 0; k < 2; ++k) {
+      if (col_on && k < zmax) cp_async8(&S.qy[k * BRICK_THREADS + t], y0p + coff0 + (long long)k * s0);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   }
 
   // ---- second and third brick axes together: warps 0-3 walk the BZ x BYX
@@ -377,7 +423,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       S.p1[s] = 0.5 * (L + R);                               // term.py:101
       S.t1[s] = ah * (R - L);                                // term.py:85-86
     };
-    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit);
+    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit, n1 - y0);
     }
   } else {
     const int y = t % BYX, z = (t - BRICK_THREADS / 2) / BYX;
@@ -391,7 +437,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       S.p2[s] = 0.5 * (L + R);
       S.t2[s] = ah * (R - L);
     };
-    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit);
+    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit, n2 - x0);
     }
   }
   __syncthreads();
@@ -421,12 +467,12 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         const long long off = off0 + (long long)i * s0;
         nz_m = need_m ? mp[off] : 0.0;
         if (AO) {
-          nz_p0 = P.aux_p0[base + off];
-          nz_d0 = P.aux_d0[base + off];
+          const double2 pd = __ldg(reinterpret_cast<const double2*>(P.aux0) + (base + off));
+          nz_p0 = pd.x;
+          nz_d0 = pd.y;
         }
       };
       fetch_node(0);
-      if constexpr (AO != 0) qy[0] = need_y0 ? y0p[coff0] : 0.0;
       auto ld = [&](int k) -> double {
         if (k < 0) return zlo[k * (BYX * BYX)];
         if (k < BZ) return col[k * PLANE];
@@ -434,19 +480,12 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       };
       auto emit = [&](int i, double L, double R) {
         if (i >= zmax) return;
-        // node i's y0 sits in slot i % QD; the slot is refilled with node i+QD.
-        // (A shift queue would move the youngest, still-loading slot every
-        // node and stall on it; the uniform switch touches one slot only.)
         double yz = 0.0;
-        const bool refill = need_y0 && i + QD < zmax && i + QD < BZ;
-        const double* nxt_y0 = y0p + (off0 + (long long)(i + QD) * s0);
-        switch (i % QD) {
-          case 0: yz = qy[0]; if (refill) qy[0] = *nxt_y0; break;
-          case 1: if constexpr (QD > 1) { yz = qy[QD > 1 ? 1 : 0]; if (refill) qy[QD > 1 ? 1 : 0] = *nxt_y0; } break;
-          case 2: if constexpr (QD > 2) { yz = qy[QD > 2 ? 2 : 0]; if (refill) qy[QD > 2 ? 2 : 0] = *nxt_y0; } break;
-          default: if constexpr (QD > 3) { yz = qy[QD - 1]; if (refill) qy[QD - 1] = *nxt_y0; } break;
+        double* qslot = &S.qy[(i & 1) * BRICK_THREADS + t];
+        if (need_y0) {
+          asm volatile("cp.async.wait_group 1;" ::: "memory");   // node i's copy has landed
+          yz = *qslot;
         }
-        static_assert(QD >= 1 && QD <= 4, "y0 prefetch depth 1..4");
         const double pv = nz_m, a0 = nz_p0, d0 = nz_d0;
         if (i + 1 < zmax && i + 1 < BZ) fetch_node(i + 1);
         const int s = s00 + i * (BYX * BYX);
@@ -482,6 +521,12 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         if (P.mask == HJ_MASK_MIN) o = (pv < o) ? pv : o;
         else if (P.mask == HJ_MASK_MAX) o = (pv > o) ? pv : o;
         out[off0 + (long long)i * s0] = o;
+        if (need_y0) {
+          // refill the slot just read with node i+2 (issued after the store of
+          // o, which consumed yz: the slot's read has completed)
+          if (i + 2 < zmax && i + 2 < BZ) cp_async8(qslot, y0p + (off0 + (long long)(i + 2) * s0));
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         // non-finite flags: finite(x) <=> |hi(x)| < 0x7FF00000
         unsigned big = max(max(abs_hi(H), abs_hi(delta)), max(abs_hi(yv), abs_hi(o)));
 #pragma unroll
@@ -497,7 +542,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
           if (!finite(o)) flags |= HJ_NF_OUTPUT;
         }
       };
-      line_walk<SCHEME, WALK_UNROLL, SEG>(ld, G.sp[AO], emit);
+      line_walk<SCHEME, WALK_UNROLL, SEG>(ld, G.sp[AO], emit, zmax);
     }
   }
 }
@@ -521,33 +566,31 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   auto emit = [&](int i, double L, double R) {
     if (i < zmax) {
       const long long o = base + (long long)(z0 + i) * plane;
-      P.aux_p0[o] = 0.5 * (L + R);                 // term.py:101
-      P.aux_d0[o] = 0.0 + ah * (R - L);            // term.py:84-86
+      // (p_avg0, d0): term.py:101, and the dissipation sum's first term (term.py:84-86)
+      reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R), 0.0 + ah * (R - L));
     }
   };
-  line_walk<SCHEME, 1, SEG>(ld, G.sp[0], emit);
+  line_walk<SCHEME, 1, SEG>(ld, G.sp[0], emit, zmax);
 }
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const size_t smem = sizeof(BrickSmem);
-  static bool configured[64] = {};  // per instantiation and device
+  static std::atomic<bool> configured[64];  // per instantiation and device (idempotent if raced)
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(k_stage_brick<SCHEME, HAM, MINB, AO, UNR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = true;
+    if (dev >= 0 && dev < 64) configured[dev].store(true, std::memory_order_release);
   }
   const GridArgs& G = P.g;
   const long long slices = AO ? (long long)G.batch * P.zp.cnt : G.batch;
   const long long nbricks = (long long)((G.n[AO + 2] + BYX - 1) / BYX) * ((G.n[AO + 1] + BYX - 1) / BYX) *
                             (AO ? (G.n[AO] + BZ - 1) / BZ : P.zr.cnt) * slices;
   if (nbricks == 0) return cudaSuccess;
-  static int sms[64] = {};
-  if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
+  const int nsm = sm_count(dev);
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
   if (AO) {
     const long long plane = G.stride[0];
@@ -565,7 +608,7 @@ template <int SCHEME, int MINB, int UNR = 1, int UNR4 = UNR>
 static cudaError_t launch_brick_ham(const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = true;
   if (P.g.dim == 4) {
-    if (!P.aux_p0 || !P.aux_d0) { *handled = false; return cudaSuccess; }
+    if (!P.aux0) { *handled = false; return cudaSuccess; }
     switch (P.ham.kind) {
       case HJ_HAM_ADVECTION: return launch_brick<SCHEME, HJ_HAM_ADVECTION, MINB, 1, UNR4>(P, s);
       case HJ_HAM_DI4: return launch_brick<SCHEME, HJ_HAM_DI4, MINB, 1, UNR4>(P, s);

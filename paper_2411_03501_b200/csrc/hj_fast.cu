@@ -12,24 +12,28 @@ cudaError_t launch_brick_weno5_fma(const StageArgs& P, cudaStream_t s, bool* han
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
 //   "brick1"        : brick-tiled WENO5 kernel compiled for 1 CTA per SM
 //   "generic"       : per-node generic kernel everywhere
-static int g_variant = -1;   // -1: take HJ_STAGE_KERNEL from the environment
+// process-wide A/B switch (set by hj_set_stage_kernel / HJ_STAGE_KERNEL);
+// atomic, read once per launch
+static std::atomic<int> g_variant{-1};   // -1: take HJ_STAGE_KERNEL from the environment
 
 static int stage_variant() {
-  if (g_variant < 0) {
+  if (g_variant.load(std::memory_order_relaxed) < 0) {
     const char* e = std::getenv("HJ_STAGE_KERNEL");
     int v = 1;
     if (e && std::string(e) == "generic") v = 0;
     if (e && std::string(e) == "brick1") v = 2;
     if (e && std::string(e) == "brick_always") v = 3;   // brick kernels even on tiny grids
     if (e && std::string(e) == "brick_u2") v = 4;       // WENO5 walks unrolled by 2
-    g_variant = v;
+    if (e && std::string(e) == "brick_noload") v = 5;   // A/B bound: tiles loaded once per CTA (wrong results)
+    int expect = -1;
+    g_variant.compare_exchange_strong(expect, v);
   }
-  return g_variant;
+  return g_variant.load(std::memory_order_relaxed);
 }
 
 int set_stage_variant(int v) {
   const int old = stage_variant();
-  g_variant = v;
+  g_variant.store(v);
   return old;
 }
 
@@ -44,14 +48,18 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
   const int ao = P.g.dim - 3;
   const long long nbricks = (long long)((P.g.n[ao + 2] + 15) / 16) * ((P.g.n[ao + 1] + 15) / 16) *
                             ((P.g.n[ao] + 7) / 8) * (ao ? (long long)P.g.n[0] : 1) * P.g.batch;
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int nsm = sm_count(dev);
+  if (variant != 3 && variant != 5 && nbricks < 2LL * nsm) return cudaSuccess;
+  if (variant == 5) {
+    // upper bound of any load-phase optimisation (TMA staging included):
+    // every brick after a CTA's first skips its global -> shared loads
+    StageArgs Q = P;
+    Q.skip_loads = 1;
+    if (scheme == HJ_WENO5) return launch_brick_weno5(Q, s, handled, 1);
+    return cudaSuccess;
   }
-  if (variant != 3 && nbricks < 2LL * nsm) return cudaSuccess;
   if (scheme == HJ_WENO5) return launch_brick_weno5(P, s, handled, variant);
   if (scheme == HJ_WENO5_FMA) return launch_brick_weno5_fma(P, s, handled, variant);
   return launch_brick_eno(scheme, P, s, handled);
@@ -59,6 +67,6 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 4) return -1;
+  if (variant < -1 || variant > 5) return -1;
   return hj::set_stage_variant(variant);
 }

@@ -1,5 +1,6 @@
 // hj_kernels.cuh -- kernel argument blocks shared by the .cu translation units.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include "hj_ham.cuh"
 
@@ -41,13 +42,14 @@ struct StageArgs {
   int want_ranges;
   int want_hnz;       // record HJ_FLAG_HAM_NONZERO (only needed when every alpha is 0)
   int tag;
+  int skip_loads;     // A/B only (stage kernel "brick_noload"): bricks after a CTA's first reuse its shared tiles
   const double* y_in;
   const double* y0;
   double* y_out;
   const double* mask_prev;
   hj_stats* stats;
-  double* aux_p0;   // 4-D brick path: axis-0 p_avg and dissipation from the pre-pass
-  double* aux_d0;
+  double* aux0;     // 4-D brick path: (p_avg0, d0) pairs per node from the axis-0 pre-pass
+                    // (interleaved: one 16-B load per node in the fused walk)
 };
 
 // Split a linear owned-node index into (problem, per-axis indices) and the
@@ -133,6 +135,22 @@ __device__ __forceinline__ void reduce_stats(hj_stats* st, unsigned flags, int t
       atomicMax((long long*)&st->hi_key[a], h);
     }
   }
+}
+
+// SM count of a device, cached per device (host side; atomic, so ranks or
+// threads driving different GPUs from one process see their own device)
+inline int sm_count(int dev) {
+  static std::atomic<int> cache[64];
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
 }
 
 constexpr long long KEY_POS_INF = 0x7ff0000000000000LL;                 // order_key(+inf)

@@ -23,7 +23,8 @@ def require():
     return _lib.load()
 
 
-STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3, "brick_u2": 4}
+STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3, "brick_u2": 4,
+                 "brick_noload": 5}   # brick_noload: A/B timing bound only, results are wrong
 
 
 def set_stage_kernel(name: str) -> str:

@@ -72,6 +72,15 @@ class FusedIntegrator:
             return self._alpha_cache
         return device_alphas(self.cfg, t, self.g, self.dg, y)
 
+    def _alphas_at(self, t: float, y: torch.Tensor | None, step: int) -> np.ndarray:
+        """_alphas inside the term evaluation of ``step``: an invalid bound (or a
+        non-finite range pass) surfaces as the reference's _rhs error
+        (integrator.py:59-63: RuntimeError 'term evaluation failed at step k')."""
+        try:
+            return self._alphas(t, y)
+        except ValueError as err:
+            raise RuntimeError(f"term evaluation failed at step {step} (t={t:g}): {err}") from err
+
     def _buffers(self, like: torch.Tensor) -> list[torch.Tensor]:
         if not self._bufs or self._bufs[0].shape != like.shape:
             self._bufs = [torch.empty_like(like) for _ in range(3)]
@@ -103,7 +112,7 @@ class FusedIntegrator:
         min_dt, max_dt = np.inf, 0.0
         zero_alpha = False
         while t < t1:
-            alphas = self._alphas(t, cur)
+            alphas = self._alphas_at(t, cur, steps)
             bound = step_bound(alphas, self.g)
             zero_alpha = zero_alpha or bound == np.inf
             dt = opts.cfl_factor * bound
@@ -132,7 +141,7 @@ class FusedIntegrator:
                 y0 = cur if kind != _lib.STAGE_EULER else None
                 if k > 0 and not self.range_free:
                     # range-dependent partials: each stage's own costate ranges (term.py:71-83)
-                    alphas_c = _lib.doubles(self._alphas(times[tag], src), _lib.HJ_MAX_DIM)
+                    alphas_c = _lib.doubles(self._alphas_at(times[tag], src, steps), _lib.HJ_MAX_DIM)
                 self._stage(alphas_c, dt, kind, src, y0, dst, mask_prev if (final and is_last) else None,
                             mask if (final and is_last) else _lib.MASK_NONE, tag, strm)
                 src = dst
@@ -186,7 +195,7 @@ class FusedIntegrator:
         one_step = False
         dt = 0.0
         if t1 > t0 and self._pipeline_ok(opts, y_host):
-            bound = step_bound(self._alphas(t0, None), self.g)
+            bound = step_bound(self._alphas_at(t0, None, 0), self.g)
             dt = opts.cfl_factor * bound
             if opts.max_step is not None:
                 dt = min(dt, opts.max_step)
@@ -301,7 +310,7 @@ class FusedIntegrator:
     def _integrate_native(self, order, t0, t1, y, opts, mask_prev, mask, use_min, check) -> DeviceIntegration:
         import ctypes
 
-        alphas = self._alphas(t0, y)
+        alphas = self._alphas_at(t0, y, 0)
         bound = step_bound(alphas, self.g)
         bufs = self._buffers(y)
         info = (ctypes.c_double * 6)()

@@ -433,9 +433,88 @@ def gen_shapes(ref, rng):
     st.save("shapes.npz")
 
 
+# plug-in contract (term.py:29-30 TermConfig callables) exercised through the
+# integrator: range-dependent partials on the rockets Hamiltonian (two-pass
+# GLF, each stage with its own costate ranges, term.py:71-83), Python-lambda
+# Hamiltonians, and the error contract of _rhs (integrator.py:59-66).
+# The formulas are restated in tests/test_gpu_plugins.py.
+def range_partials(ref, params):
+    def partials(t, g, v, ranges, i):
+        base = ref.rockets_partials(t, g, v, ranges, i, params)
+        return base + 0.01 * (abs(ranges[i][0]) + abs(ranges[i][1]))
+    return partials
+
+
+def lambda_ham(t, g, v, p):
+    # a nonlinear Hamiltonian written the way the reference's tests write them
+    x = np.asarray(g.axis_nodes[0]).reshape((-1,) + (1,) * (g.dim - 1))
+    h = 0.5 * p[0].values * p[0].values - 0.25 * p[1].values + 0.1 * x * p[g.dim - 1].values
+    return type(p[0])(h)
+
+
+def lambda_partials(t, g, v, ranges, i):
+    return max(abs(ranges[i][0]), abs(ranges[i][1])) + 0.5
+
+
+def gen_plugins(ref, rng):
+    st = Store()
+    params = ref.RocketParams()
+    spec = gspec((-64.0, -64.0, -math.pi), (64.0, 64.0, math.pi), (9, 8, 10), periodic={2})
+    g = make_grid(ref, spec)
+    target = ref.cylinder(g, 2, (0.0, 0.0, 0.0), 15.0)
+    for scheme in ("eno2", "weno5"):
+        base = ref.rockets_term_config(params, scheme=scheme)
+        cfg = ref.TermConfig(hamiltonian=base.hamiltonian, partials=range_partials(ref, params),
+                             derivative_scheme=scheme)
+        res = ref.ode_cfl_3(lambda t, y, c: ref.term_lax_friedrichs(t, y, c, g), (0.0, 0.05), target,
+                            ref.IntegratorOptions(cfl_factor=0.5), cfg)
+        st.case(dict(kind="rockets_range_partials", grid=spec, scheme=scheme, t1=0.05), y0=target.values,
+                y=res.y_final.values, info=np.array([res.t_final, res.steps_taken, res.min_dt, res.max_dt]),
+                cos=np.cos(g.axis_nodes[2].reshape(1, 1, -1)).ravel(),
+                sin=np.sin(g.axis_nodes[2].reshape(1, 1, -1)).ravel())
+    spec2 = gspec((-1.0, -1.0), (1.0, 2.0), (12, 14), periodic={1})
+    g2 = make_grid(ref, spec2)
+    y0 = np.sin(np.pi * ref_mesh(g2, 0)) * np.cos(ref_mesh(g2, 1)) + 0.1 * ref_mesh(g2, 1)
+    for scheme in ("first", "eno3", "weno5"):
+        cfg = ref.TermConfig(hamiltonian=lambda_ham, partials=lambda_partials, derivative_scheme=scheme)
+        res = ref.ode_cfl_3(lambda t, y, c: ref.term_lax_friedrichs(t, y, c, g2), (0.0, 0.08),
+                            ref.ScalarField(y0), ref.IntegratorOptions(cfl_factor=0.4), cfg)
+        st.case(dict(kind="lambda_ham", grid=spec2, scheme=scheme, t1=0.08, cfl=0.4), y0=y0,
+                y=res.y_final.values, info=np.array([res.t_final, res.steps_taken, res.min_dt, res.max_dt]))
+    # the error contract: what the reference raises, verbatim
+    errs = {
+        "invalid_bound": ref.TermConfig(hamiltonian=lambda_ham, partials=lambda *a: -1.0, derivative_scheme="eno2"),
+        "nan_hamiltonian": ref.TermConfig(hamiltonian=lambda t, g, v, p: np.full(p[0].values.shape, np.nan),
+                                          partials=lambda *a: 1.0, derivative_scheme="eno2"),
+    }
+    for name, cfg in errs.items():
+        try:
+            ref.ode_cfl_3(lambda t, y, c: ref.term_lax_friedrichs(t, y, c, g2), (0.0, 0.08), ref.ScalarField(y0),
+                          ref.IntegratorOptions(cfl_factor=0.4), cfg)
+            raise AssertionError(f"{name}: the reference did not raise")
+        except (RuntimeError, ValueError) as err:
+            st.case(dict(kind="error", name=name, grid=spec2, error=type(err).__name__, message=str(err)), y0=y0)
+    # the same invalid bound on a REGISTERED Hamiltonian (rockets), range-dependent partials
+    base = ref.rockets_term_config(params, scheme="eno2")
+    cfg = ref.TermConfig(hamiltonian=base.hamiltonian, partials=lambda t, g, v, r, i: -2.0 if i == 1 else 1.0,
+                         derivative_scheme="eno2")
+    try:
+        ref.ode_cfl_3(lambda t, y, c: ref.term_lax_friedrichs(t, y, c, g), (0.0, 0.05), target,
+                      ref.IntegratorOptions(), cfg)
+        raise AssertionError("rockets invalid bound: the reference did not raise")
+    except (RuntimeError, ValueError) as err:
+        st.case(dict(kind="error", name="rockets_invalid_bound", grid=spec, error=type(err).__name__,
+                     message=str(err)), y0=target.values, cos=np.cos(g.axis_nodes[2].reshape(1, 1, -1)).ravel(),
+                sin=np.sin(g.axis_nodes[2].reshape(1, 1, -1)).ravel())
+    st.save("plugins.npz")
+
+
 def main():
     root = sys.argv[1] if len(sys.argv) > 1 else "/root/reference"
     ref = load_reference(root)
+    if len(sys.argv) > 2:   # e.g. `make_golden.py /root/reference plugins`: one generator only
+        globals()[f"gen_{sys.argv[2]}"](ref, np.random.default_rng(20241103))
+        return
     rng = np.random.default_rng(20241103)
     gen_grid_and_ghost(ref, rng)
     gen_derivs(ref, rng)
@@ -445,6 +524,7 @@ def main():
     gen_integrate(ref, rng)
     gen_brt(ref, rng)
     gen_shapes(ref, rng)
+    gen_plugins(ref, np.random.default_rng(20241103))
 
 
 if __name__ == "__main__":
