@@ -277,8 +277,9 @@ int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, 
  * kernel, 1 brick kernels when the grid has enough bricks (default), 2 brick
  * WENO5 kernel at 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid, 4 WENO5
  * walks rolled, 5 timing bound only (WENO5 bricks after a CTA's first skip
- * their global->shared loads: WRONG results); -1 reads HJ_STAGE_KERNEL from
- * the environment.  Returns the previous setting. */
+ * their global->shared loads: WRONG results), 6 brick kernels without the L2
+ * prefetch of the next brick; -1 reads HJ_STAGE_KERNEL from the environment.
+ * Returns the previous setting. */
 int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
  * iters x 8 independent DFMA chains (time it with events on `stream`). */

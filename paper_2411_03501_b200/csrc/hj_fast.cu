@@ -25,6 +25,7 @@ static int stage_variant() {
     if (e && std::string(e) == "brick_always") v = 3;   // brick kernels even on tiny grids
     if (e && std::string(e) == "brick_u2") v = 4;       // WENO5 walks unrolled by 2
     if (e && std::string(e) == "brick_noload") v = 5;   // A/B bound: tiles loaded once per CTA (wrong results)
+    if (e && std::string(e) == "brick_nopf") v = 6;     // A/B: no L2 prefetch of the next brick
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
@@ -52,6 +53,13 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
   cudaGetDevice(&dev);
   const int nsm = sm_count(dev);
   if (variant != 3 && variant != 5 && nbricks < 2LL * nsm) return cudaSuccess;
+  if (variant == 6) {
+    StageArgs Q = P;
+    Q.no_prefetch = 1;
+    if (scheme == HJ_WENO5) return launch_brick_weno5(Q, s, handled, 1);
+    if (scheme == HJ_WENO5_FMA) return launch_brick_weno5_fma(Q, s, handled, 1);
+    return launch_brick_eno(scheme, Q, s, handled);
+  }
   if (variant == 5) {
     // upper bound of any load-phase optimisation (TMA staging included):
     // every brick after a CTA's first skips its global -> shared loads
@@ -67,6 +75,6 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 5) return -1;
+  if (variant < -1 || variant > 6) return -1;
   return hj::set_stage_variant(variant);
 }

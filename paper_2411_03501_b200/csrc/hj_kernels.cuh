@@ -43,6 +43,7 @@ struct StageArgs {
   int want_hnz;       // record HJ_FLAG_HAM_NONZERO (only needed when every alpha is 0)
   int tag;
   int skip_loads;     // A/B only (stage kernel "brick_noload"): bricks after a CTA's first reuse its shared tiles
+  int no_prefetch;    // A/B only (stage kernel "brick_nopf"): no L2 prefetch of the next brick
   const double* y_in;
   const double* y0;
   double* y_out;

@@ -24,7 +24,8 @@ def require():
 
 
 STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3, "brick_u2": 4,
-                 "brick_noload": 5}   # brick_noload: A/B timing bound only, results are wrong
+                 "brick_noload": 5,   # brick_noload: A/B timing bound only, results are wrong
+                 "brick_nopf": 6}     # no L2 prefetch of the next brick (A/B)
 
 
 def set_stage_kernel(name: str) -> str:
