@@ -419,32 +419,57 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   // (lines whose nodes all lie outside the domain -- the partial bricks at
   // the far faces -- are skipped: nothing reads their p_avg / dissipation,
   // and the FP64 pipe they would occupy is shared with the SM's other warps)
-  if (t < BRICK_THREADS / 2) {
+  // 4-D: one code path serves both walks (line stride, output arrays and the
+  // swizzled slot are runtime selects), so the two walk loops share one copy
+  // in the instruction cache; each warp is wholly a y- or an x-walk warp
+  // (measured: +3.7 % on 121^4; the 3-D kernel keeps two specialised copies,
+  // -1.6 % there from the extra registers)
+  if constexpr (AO == 1) {
+    const bool yw = t < BRICK_THREADS / 2;
+    const int tt = yw ? t : t - BRICK_THREADS / 2;
+    const int c = tt % BYX, z = tt / BYX;   // c: the line's x (y-walk) or y (x-walk)
+    if (z0 + z < n0 && (yw ? x0 + c < n2 : y0 + c < n1)) {
+      const double* line = yw ? &S.v[z * PLANE + HB * SVP + (c + HB)] : &S.v[z * PLANE + (c + HB) * SVP + HB];
+      const int step = yw ? SVP : 1;
+      const double ah = P.alpha_half[AO + (yw ? 1 : 2)];
+      double* pa = yw ? S.p1 : S.p2;
+      double* ta = yw ? S.t1 : S.t2;
+      const int row = z * BYX * BYX;
+      auto ld = [&](int k) -> double { return line[k * step]; };
+      auto emit = [&](int i, double L, double R) {
+        // swz(z, i, c) for the y-walk, swz(z, c, i) for the x-walk
+        const int s = row + (yw ? i * BYX + (c ^ i) : c * BYX + (i ^ c));
+        pa[s] = 0.5 * (L + R);                               // term.py:101
+        ta[s] = ah * (R - L);                                // term.py:85-86
+      };
+      line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + (yw ? 1 : 2)], emit, yw ? n1 - y0 : n2 - x0);
+    }
+  } else if (t < BRICK_THREADS / 2) {
     const int x = t % BYX, z = t / BYX;
     if (z0 + z < n0 && x0 + x < n2) {
-    const double* line = &S.v[z * PLANE + HB * SVP + (x + HB)];
-    const double ah = P.alpha_half[AO + 1];
-    auto ld = [&](int k) -> double { return line[k * SVP]; };
-    auto emit = [&](int i, double L, double R) {
-      const int s = swz(z, i, x);
-      S.p1[s] = 0.5 * (L + R);                               // term.py:101
-      S.t1[s] = ah * (R - L);                                // term.py:85-86
-    };
-    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit, n1 - y0);
+      const double* line = &S.v[z * PLANE + HB * SVP + (x + HB)];
+      const double ah = P.alpha_half[AO + 1];
+      auto ld = [&](int k) -> double { return line[k * SVP]; };
+      auto emit = [&](int i, double L, double R) {
+        const int s = swz(z, i, x);
+        S.p1[s] = 0.5 * (L + R);                               // term.py:101
+        S.t1[s] = ah * (R - L);                                // term.py:85-86
+      };
+      line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 1], emit, n1 - y0);
     }
   } else {
     const int y = t % BYX, z = (t - BRICK_THREADS / 2) / BYX;
     if (z0 + z < n0 && y0 + y < n1) {
-    const double* line = &S.v[z * PLANE + (y + HB) * SVP + HB];
-    const double ah = P.alpha_half[AO + 2];
-    const int row = (z * BYX + y) * BYX;
-    auto ld = [&](int k) -> double { return line[k]; };
-    auto emit = [&](int i, double L, double R) {
-      const int s = row + (i ^ y);
-      S.p2[s] = 0.5 * (L + R);
-      S.t2[s] = ah * (R - L);
-    };
-    line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit, n2 - x0);
+      const double* line = &S.v[z * PLANE + (y + HB) * SVP + HB];
+      const double ah = P.alpha_half[AO + 2];
+      const int row = (z * BYX + y) * BYX;
+      auto ld = [&](int k) -> double { return line[k]; };
+      auto emit = [&](int i, double L, double R) {
+        const int s = row + (i ^ y);
+        S.p2[s] = 0.5 * (L + R);
+        S.t2[s] = ah * (R - L);
+      };
+      line_walk<SCHEME, WALK_UNROLL, LSEG>(ld, G.sp[AO + 2], emit, n2 - x0);
     }
   }
   __syncthreads();
