@@ -195,14 +195,17 @@ def sass_hash(symbol: str) -> str | None:
                              text=True, timeout=120).stdout
     except Exception:
         return None
+    import re
+
     h = hashlib.sha256()
     n = 0
     for line in out.splitlines():
-        body = line.split("/*")[0].strip() if "/*" in line else line.strip()
-        if body and not body.startswith(("Fatbin", "code for", "arch =", "host =", "compile_size", "=====")):
+        # "/*0a30*/   DFMA R4, R2, R6, R8 ;   /* 0x... */": keep the instruction text only
+        body = re.sub(r"/\*[^*]*\*/", "", line).strip()
+        if re.match(r"^[@A-Z]", body) and not body.startswith(("Fatbin", "Function")):
             h.update(body.encode())
             n += 1
-    return h.hexdigest() if n else None
+    return h.hexdigest() if n > 100 else None
 
 
 def brick_symbol(frag: str) -> str:

@@ -265,28 +265,36 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       // boundary brick, phase 1: every value that lives in memory (in-domain,
       // periodic wrap, exchanged halo planes) goes through cp.async; the
       // extrapolated / dirichlet ghosts wait for their edge nodes (phase 2)
-      const int jx = ghost_index(A2, gx);
+      // (slots no walk reads -- outside the domain on both walk axes, planes
+      // beyond the exchanged halos -- are left untouched)
+      const int jx = gx_in ? gx : ghost_index(A2, gx);   // this lane's column: in memory or GI_SYNTH
       const int jz = ghost_index(A0, gz);
-      for (int yy = 0; yy < SVR; ++yy, srow += SVP) {
-        const bool yin = yy >= HB && yy < HB + BYX;
-        if (!lane_on || !(yin || xin)) continue;
-        const int gy = y0 + yy - HB;
-        const bool gy_in = gy >= 0 && gy < n1;
-        if (gz < n0) {
-          if (!gy_in && !gx_in) {
-            *srow = 0.0;   // outside the domain on both walk axes: never read
-          } else {
-            const int jy = gy_in ? gy : ghost_index(A1, gy);
-            const int jxx = gx_in ? gx : jx;
-            if (jy != GI_SYNTH && jxx != GI_SYNTH) cp_async8(srow, vin + (gz * s0 + jy * s1 + jxx));
+      const bool xmem = lane_on && jx != GI_SYNTH;
+      const int r_lo = max(0, HB - y0), r_hi = min(SVR, n1 - y0 + HB);   // rows with gy in the domain
+      if (gz < n0) {
+        if (xmem) {
+          // in-domain rows: one incrementing row pointer, as on interior bricks
+          const double* grow = vin + ((long long)gz * s0 + (long long)(y0 - HB + r_lo) * s1 + jx);
+          double* dst = &S.v[z * PLANE + r_lo * SVP + lane];
+          for (int yy = r_lo; yy < r_hi; ++yy, grow += s1, dst += SVP)
+            if (xin || (yy >= HB && yy < HB + BYX)) cp_async8(dst, grow);
+          // ghost rows of a periodic second axis (their images live in memory),
+          // read by the second-axis walk at the brick's own columns only
+          if (A1.bc == HJ_BC_PERIODIC && xin && (r_lo > 0 || r_hi < SVR)) {
+            for (int yy = 0; yy < SVR; ++yy) {
+              if (yy >= r_lo && yy < r_hi) continue;
+              const int jy = ghost_index(A1, y0 + yy - HB);
+              cp_async8(&S.v[z * PLANE + yy * SVP + lane], vin + ((long long)gz * s0 + (long long)jy * s1 + jx));
+            }
           }
-        } else if (gy_in && gx_in) {
-          // beyond the last plane of a partial brick: first-axis ghosts (read by the first-axis walk)
-          if (jz == GI_ZERO) *srow = 0.0;
-          else if (jz != GI_SYNTH) cp_async8(srow, vin + ((long long)jz * s0 + gy * s1 + gx));
-        } else {
-          *srow = 0.0;   // never read
         }
+      } else if (jz != GI_SYNTH && jz != GI_ZERO && xin && gx_in) {
+        // beyond the last plane of a partial brick, a plane that lives in memory
+        // (periodic image / exchanged halo): the first-axis walk's columns
+        const int ya = max(r_lo, HB), yb = min(r_hi, HB + BYX);
+        const double* grow = vin + ((long long)jz * s0 + (long long)(y0 - HB + ya) * s1 + gx);
+        double* dst = &S.v[z * PLANE + ya * SVP + lane];
+        for (int yy = ya; yy < yb; ++yy, grow += s1, dst += SVP) cp_async8(dst, grow);
       }
       // first-axis halo planes (interior rows and columns of the brick only)
       const int half = lane >> 4, xl = lane & (BYX - 1);
