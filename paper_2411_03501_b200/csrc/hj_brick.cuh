@@ -588,29 +588,53 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
 }
 
 // ---- 4-D pre-pass: the axis-0 walks (one thread per column segment, coalesced
-// across the last axis); p_avg0 and d0 = 0 + (alpha0*0.5)*(R0-L0) to scratch
+// across the last axis); p_avg0 and d0 = 0 + (alpha0*0.5)*(R0-L0) to scratch.
+// A segment covers up to PRE_ROWS consecutive 8-plane rows of the launch's
+// row set (zr: rows lo..lo+split-1, then hs..): longer segments amortise the
+// walk's window fill (5 faces + 3 centres) over more nodes.
+constexpr int PRE_ROWS = 2;
+constexpr int PRE_SEG = PRE_ROWS * SEG;   // 16 nodes
+
+__host__ __device__ __forceinline__ int pre_segments(const RowSet& r) {
+  return (r.split + PRE_ROWS - 1) / PRE_ROWS + (r.cnt - r.split + PRE_ROWS - 1) / PRE_ROWS;
+}
+
 template <int SCHEME>
 __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   const GridArgs& G = P.g;
   const long long plane = G.stride[0];
   const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= plane) return;
-  const int seg = P.zr.map(blockIdx.y % P.zr.cnt), pb = blockIdx.y / P.zr.cnt;
-  const int z0 = seg * SEG;
+  const RowSet& R = P.zr;
+  const int nseg = pre_segments(R);
+  const int sidx = blockIdx.y % nseg, pb = blockIdx.y / nseg;
+  const int na = (R.split + PRE_ROWS - 1) / PRE_ROWS;
+  int row, rows;   // first row of the segment and its row count
+  if (sidx < na) {
+    row = R.lo + sidx * PRE_ROWS;
+    rows = min(PRE_ROWS, R.split - sidx * PRE_ROWS);
+  } else {
+    const int k = sidx - na;
+    row = R.hs + k * PRE_ROWS;
+    rows = min(PRE_ROWS, (R.cnt - R.split) - k * PRE_ROWS);
+  }
+  const int z0 = row * SEG;
   const long long base = (long long)pb * G.batch_stride + pos;
   const double* col = P.y_in + base;
   const AxisView A0 = G.ax[0];
   const double ah = P.alpha_half[0];
-  const int zmax = G.n[0] - z0;
-  auto ld = [&](int k) -> double { return fetch(col, A0, z0 + k); };
-  auto emit = [&](int i, double L, double R) {
+  const int zmax = min(rows * SEG, G.n[0] - z0);
+  // a segment whose stencils stay inside the owned planes loads directly
+  const bool inner = z0 >= 3 && z0 + zmax + 3 <= G.n[0];
+  auto ld = [&](int k) -> double { return inner ? col[(long long)(z0 + k) * plane] : fetch(col, A0, z0 + k); };
+  auto emit = [&](int i, double L, double R2) {
     if (i < zmax) {
       const long long o = base + (long long)(z0 + i) * plane;
       // (p_avg0, d0): term.py:101, and the dissipation sum's first term (term.py:84-86)
-      reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R), 0.0 + ah * (R - L));
+      reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R2), 0.0 + ah * (R2 - L));
     }
   };
-  line_walk<SCHEME, 1, SEG>(ld, G.sp[0], emit, zmax);
+  line_walk<SCHEME, 1, PRE_SEG>(ld, G.sp[0], emit, zmax);
 }
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
@@ -634,7 +658,7 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
   if (AO) {
     const long long plane = G.stride[0];
-    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(P.zr.cnt * G.batch));
+    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments(P.zr) * G.batch));
     k_axis0_walk<SCHEME><<<pg, 256, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -45,10 +45,28 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
           uu[a][k] = 0.0;
       }
     }
+    // ENO / first-order: every axis' quotients on the branch-free fast path
+    // (independent chains the scheduler can interleave), one rarely taken
+    // exact redo of the node; WENO5 keeps its per-division form here
+    LR lrs[DIM];
+    constexpr bool kFast = SCHEME == HJ_FIRST || SCHEME == HJ_ENO2 || SCHEME == HJ_ENO3;
+    bool ok = kFast;
+    if constexpr (kFast) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const EnoRecips K = eno_recips(P.g.sp[a]);
+        if (SCHEME == HJ_FIRST) lrs[a] = scheme_first_q(uu[a], K, ok);
+        else if (SCHEME == HJ_ENO2) lrs[a] = scheme_eno2_q(uu[a], P.g.sp[a], K, ok);
+        else lrs[a] = scheme_eno3_q(uu[a], P.g.sp[a], K, ok);
+      }
+    }
+    if (!ok) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) lrs[a] = scheme_lr<SCHEME>(uu[a], P.g.sp[a], P.eps_mode);
+    }
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-      const double* u = uu[a];
-      const LR lr = scheme_lr<SCHEME>(u, P.g.sp[a], P.eps_mode);
+      const LR lr = lrs[a];
       if (!finite(lr.l) || !finite(lr.r)) flags |= HJ_NF_DERIV;
       if (P.want_ranges) {
         lo[a] = min(order_key(lr.l), order_key(lr.r));
