@@ -209,9 +209,11 @@ def sass_hash(symbol: str) -> str | None:
 
 
 def brick_symbol(frag: str) -> str:
-    """'k_stage_brickILi3ELi3ELi2ELi0ELi2EE' -> the kernel's mangled symbol"""
+    """'k_stage_brickILi3ELi3ELi2ELi0ELi2EE' -> the kernel's mangled symbol
+    (k_stage_brick(StageArgs, int); k_stage_generic(StageArgs))"""
     base = frag.split("I", 1)[0]
-    return f"_ZN2hj{len(base)}{frag}EvNS_9StageArgsEi"
+    args = "NS_9StageArgsEi" if base == "k_stage_brick" else "NS_9StageArgsE"
+    return f"_ZN2hj{len(base)}{frag}Ev{args}"
 
 
 def fp64_ops(key: str):
@@ -224,6 +226,8 @@ def fp64_ops(key: str):
     except Exception:
         return None, "no profiles/fp64_ops.json"
     ent = d.get(key)
+    if not isinstance(ent, dict) and key.startswith("c3_"):
+        ent = d.get("c2_" + key[3:])   # C3 runs the C2 kernel (same instantiation; the SASS hash is checked)
     if not isinstance(ent, dict):
         return None, f"no entry {key}"
     now = sass_hash(ent.get("symbol", ""))

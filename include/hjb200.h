@@ -284,6 +284,12 @@ int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
  * iters x 8 independent DFMA chains (time it with events on `stream`). */
 int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream);
+/* Bounds-checking build only (libhjb200_check.so, compiled with
+ * -DHJ_CHECK_BOUNDS; compute-sanitizer is closed on this pool): global
+ * accesses of the stage kernels outside the extents of their fields since
+ * the last call (synchronises the device, resets the count); -1 in the
+ * normal build. */
+int64_t hj_bounds_violations(void);
 /* zero a device hj_stats (keys set to +inf/-inf images) */
 int hj_stats_reset(hj_stats* stats, void* stream);
 

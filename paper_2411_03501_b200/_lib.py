@@ -74,6 +74,9 @@ STATS_BYTES = ctypes.sizeof(HjStats)
 
 _LIB = None
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhjb200.so")
+# HJ_LIB=check selects the bounds-checking build (libhjb200_check.so, build.py --check)
+if os.environ.get("HJ_LIB") == "check":
+    _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhjb200_check.so")
 
 # (name, restype, argtypes) -- must match include/hjb200.h
 _SIGNATURES = [
@@ -103,6 +106,7 @@ _SIGNATURES = [
     ("hj_mask", c_int, [c_int64, c_void_p, c_void_p, c_int, c_void_p]),
     ("hj_count_below", c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     ("hj_stats_reset", c_int, [c_void_p, c_void_p]),
+    ("hj_bounds_violations", c_int64, []),
     ("hj_eval_hamiltonian", c_int, [POINTER(HjGrid), POINTER(HjHam), POINTER(c_void_p), c_void_p, c_void_p]),
     ("hj_integrate", c_int, [POINTER(HjGrid), c_int, POINTER(HjHam), POINTER(c_double), c_int, c_double, c_double,
                              c_double, c_double, c_int, c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -37,10 +37,10 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src: str, verbose: bool, check: bool = False) -> str:
+    obj = os.path.join(OBJ + ("_check" if check else ""), os.path.basename(src)[:-3] + ".o")
     if _stale(obj, [src, *_deps()]):
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DHJ_CHECK_BOUNDS"] if check else []), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -49,23 +49,27 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
-    """Compile (incrementally) and link libhjb200.so; returns its path."""
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, jobs: int | None = None, check: bool = False) -> str:
+    """Compile (incrementally) and link libhjb200.so; returns its path.
+    check=True builds libhjb200_check.so instead: the same kernels with every
+    global access of the stage kernels tested against its field's extent
+    (-DHJ_CHECK_BOUNDS; tests and scripts/bounds_check.py only)."""
+    os.makedirs(OBJ + ("_check" if check else ""), exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = jobs or max(1, min(len(sources), os.cpu_count() or 1))
     with cf.ThreadPoolExecutor(jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources))
-    if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB + ".tmp"]
+        objs = list(ex.map(lambda s: _compile(s, verbose, check), sources))
+    lib = LIB.replace(".so", "_check.so") if check else LIB
+    if _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", lib + ".tmp"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, check="--check" in sys.argv))

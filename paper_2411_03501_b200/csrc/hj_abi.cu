@@ -214,6 +214,43 @@ static double* scratch_for(cudaStream_t s, size_t n_doubles) {
   return e->p;
 }
 
+// ---- bounds checking (libhjb200_check.so, -DHJ_CHECK_BOUNDS): the extents of
+// the fields a stage touches and a per-device violation counter
+#ifdef HJ_CHECK_BOUNDS
+static unsigned long long* oob_counter() {
+  static std::mutex mu;
+  static unsigned long long* per_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!per_dev[dev]) {
+    if (cudaMalloc((void**)&per_dev[dev], sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(per_dev[dev], 0, sizeof(unsigned long long));
+  }
+  return per_dev[dev];
+}
+#endif
+
+static void set_extents(StageArgs& P, const hj_grid* g) {
+  const GridArgs& G = P.g;
+  long long plane = 1;
+  for (int a = 1; a < G.dim; ++a) plane *= G.n[a];
+  const long long span = G.batch_stride * (G.batch - 1) + G.cells;
+  const long long below = g->halo_lo ? (long long)g->halo * plane : 0;
+  const long long above = g->halo_hi ? (long long)g->halo * plane : 0;
+  P.bc.in = Extent{P.y_in - below, P.y_in + span + above};
+  P.bc.y0 = Extent{P.y0, P.y0 ? P.y0 + span : nullptr};
+  P.bc.out = Extent{P.y_out, P.y_out + span};
+  P.bc.mask = Extent{P.mask_prev, P.mask_prev ? P.mask_prev + span : nullptr};
+  P.bc.aux = Extent{P.aux0, P.aux0 ? P.aux0 + 2 * span : nullptr};
+#ifdef HJ_CHECK_BOUNDS
+  P.bc.oob = oob_counter();
+#else
+  P.bc.oob = nullptr;
+#endif
+}
+
 // Derived constants computed once on the host side of the ABI.
 static hj_ham prep_ham(const hj_ham* ham) {
   hj_ham h = *ham;
@@ -359,6 +396,7 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
       P.aux0 = scratch;   // span (p_avg0, d0) pairs
     }
   }
+  set_extents(P, g);
   bool handled = false;
   cudaError_t e = launch_stage_fast(scheme, P, s, &handled);
   if (!handled) e = launch_stage_generic(scheme, P, s);
@@ -415,6 +453,7 @@ int hj_term(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha
   P.y_in = v;
   P.y_out = delta;
   P.stats = stats;
+  set_extents(P, g);
   return cuda_status(launch_stage_generic(scheme, P, (cudaStream_t)stream), "hj_term");
 }
 
@@ -514,6 +553,20 @@ int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, 
 int hj_fp64_probe(int iters, int blocks, double* d_sink, void* stream) {
   if (iters < 1 || blocks < 1 || !d_sink) return fail(HJ_EINVAL, "bad arguments");
   return cuda_status(launch_fp64_probe(iters, blocks, d_sink, (cudaStream_t)stream), "hj_fp64_probe");
+}
+
+int64_t hj_bounds_violations(void) {
+#ifdef HJ_CHECK_BOUNDS
+  unsigned long long* c = oob_counter();
+  if (!c) return fail(HJ_ECUDA, "bounds counter unavailable");
+  unsigned long long n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(&n, c, sizeof n, cudaMemcpyDeviceToHost);
+  cudaMemset(c, 0, sizeof n);
+  return (int64_t)n;
+#else
+  return -1;
+#endif
 }
 
 int hj_stats_reset(hj_stats* stats, void* stream) {

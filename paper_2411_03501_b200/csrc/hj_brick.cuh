@@ -259,7 +259,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
 #pragma unroll 2
       for (int yy = 0; yy < SVR; ++yy, grow += s1, srow += SVP) {
         const bool yin = yy >= HB && yy < HB + BYX;
-        if (lane_on && (yin || xin)) cp_async8(srow, grow);
+        if (lane_on && (yin || xin)) { HJ_CHK(P, in, grow, 8); cp_async8(srow, grow); }
       }
     } else {
       // boundary brick, phase 1: every value that lives in memory (in-domain,
@@ -277,14 +277,16 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
           const double* grow = vin + ((long long)gz * s0 + (long long)(y0 - HB + r_lo) * s1 + jx);
           double* dst = &S.v[z * PLANE + r_lo * SVP + lane];
           for (int yy = r_lo; yy < r_hi; ++yy, grow += s1, dst += SVP)
-            if (xin || (yy >= HB && yy < HB + BYX)) cp_async8(dst, grow);
+            if (xin || (yy >= HB && yy < HB + BYX)) { HJ_CHK(P, in, grow, 8); cp_async8(dst, grow); }
           // ghost rows of a periodic second axis (their images live in memory),
           // read by the second-axis walk at the brick's own columns only
           if (A1.bc == HJ_BC_PERIODIC && xin && (r_lo > 0 || r_hi < SVR)) {
             for (int yy = 0; yy < SVR; ++yy) {
               if (yy >= r_lo && yy < r_hi) continue;
               const int jy = ghost_index(A1, y0 + yy - HB);
-              cp_async8(&S.v[z * PLANE + yy * SVP + lane], vin + ((long long)gz * s0 + (long long)jy * s1 + jx));
+              const double* src = vin + ((long long)gz * s0 + (long long)jy * s1 + jx);
+              HJ_CHK(P, in, src, 8);
+              cp_async8(&S.v[z * PLANE + yy * SVP + lane], src);
             }
           }
         }
@@ -294,7 +296,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         const int ya = max(r_lo, HB), yb = min(r_hi, HB + BYX);
         const double* grow = vin + ((long long)jz * s0 + (long long)(y0 - HB + ya) * s1 + gx);
         double* dst = &S.v[z * PLANE + ya * SVP + lane];
-        for (int yy = ya; yy < yb; ++yy, grow += s1, dst += SVP) cp_async8(dst, grow);
+        for (int yy = ya; yy < yb; ++yy, grow += s1, dst += SVP) {
+          HJ_CHK(P, in, grow, 8);
+          cp_async8(dst, grow);
+        }
       }
       // first-axis halo planes (interior rows and columns of the brick only)
       const int half = lane >> 4, xl = lane & (BYX - 1);
@@ -307,7 +312,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         const int gy = y0 + y, gxx = x0 + xl;
         double* dst = &S.zh[row * BYX + xl];
         if (gy >= n1 || gxx >= n2 || je == GI_ZERO) *dst = 0.0;
-        else if (je != GI_SYNTH) cp_async8(dst, vin + ((long long)je * s0 + gy * s1 + gxx));
+        else if (je != GI_SYNTH) {
+          HJ_CHK(P, in, vin + ((long long)je * s0 + gy * s1 + gxx), 8);
+          cp_async8(dst, vin + ((long long)je * s0 + gy * s1 + gxx));
+        }
       }
       cp_async_wait_all();
       __syncthreads();
@@ -377,6 +385,7 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         const int row = 2 * r2 + half;
         const int k = row / BYX, y = row % BYX;
         const int e = (k < HB) ? (z0 - HB + k) : (z0 + BZ + k - HB);
+        HJ_CHK(P, in, vin + e * s0 + (y0 + y) * s1 + (x0 + xl), 8);
         cp_async8(&S.zh[row * BYX + xl], vin + e * s0 + (y0 + y) * s1 + (x0 + xl));
       }
     }
@@ -416,7 +425,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
   if (need_y0) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      if (col_on && k < zmax) cp_async8(&S.qy[k * BRICK_THREADS + t], y0p + coff0 + (long long)k * s0);
+      if (col_on && k < zmax) {
+        HJ_CHK(P, y0, y0p + coff0 + (long long)k * s0, 8);
+        cp_async8(&S.qy[k * BRICK_THREADS + t], y0p + coff0 + (long long)k * s0);
+      }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   }
@@ -505,8 +517,10 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
       double nz_m = 0.0, nz_p0 = 0.0, nz_d0 = 0.0;
       auto fetch_node = [&](int i) {
         const long long off = off0 + (long long)i * s0;
+        if (need_m) HJ_CHK(P, mask, mp + off, 8);
         nz_m = need_m ? mp[off] : 0.0;
         if (AO) {
+          HJ_CHK(P, aux, reinterpret_cast<const double2*>(P.aux0) + (base + off), 16);
           const double2 pd = __ldg(reinterpret_cast<const double2*>(P.aux0) + (base + off));
           nz_p0 = pd.x;
           nz_d0 = pd.y;
@@ -560,11 +574,15 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
         double o = stage_update(P.stage, P.dt, yv, yz, delta);
         if (P.mask == HJ_MASK_MIN) o = (pv < o) ? pv : o;
         else if (P.mask == HJ_MASK_MAX) o = (pv > o) ? pv : o;
+        HJ_CHK(P, out, out + off0 + (long long)i * s0, 8);
         out[off0 + (long long)i * s0] = o;
         if (need_y0) {
           // refill the slot just read with node i+2 (issued after the store of
           // o, which consumed yz: the slot's read has completed)
-          if (i + 2 < zmax && i + 2 < BZ) cp_async8(qslot, y0p + (off0 + (long long)(i + 2) * s0));
+          if (i + 2 < zmax && i + 2 < BZ) {
+            HJ_CHK(P, y0, y0p + (off0 + (long long)(i + 2) * s0), 8);
+            cp_async8(qslot, y0p + (off0 + (long long)(i + 2) * s0));
+          }
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
         // non-finite flags: finite(x) <=> |hi(x)| < 0x7FF00000
@@ -626,11 +644,15 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   const int zmax = min(rows * SEG, G.n[0] - z0);
   // a segment whose stencils stay inside the owned planes loads directly
   const bool inner = z0 >= 3 && z0 + zmax + 3 <= G.n[0];
-  auto ld = [&](int k) -> double { return inner ? col[(long long)(z0 + k) * plane] : fetch(col, A0, z0 + k); };
+  auto ld = [&](int k) -> double {
+    if (inner) HJ_CHK(P, in, col + (long long)(z0 + k) * plane, 8);
+    return inner ? col[(long long)(z0 + k) * plane] : fetch(col, A0, z0 + k);
+  };
   auto emit = [&](int i, double L, double R2) {
     if (i < zmax) {
       const long long o = base + (long long)(z0 + i) * plane;
       // (p_avg0, d0): term.py:101, and the dissipation sum's first term (term.py:84-86)
+      HJ_CHK(P, aux, reinterpret_cast<double2*>(P.aux0) + o, 16);
       reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R2), 0.0 + ah * (R2 - L));
     }
   };

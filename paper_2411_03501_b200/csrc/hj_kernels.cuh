@@ -1,6 +1,7 @@
 // hj_kernels.cuh -- kernel argument blocks shared by the .cu translation units.
 #pragma once
 #include <atomic>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include "hj_ham.cuh"
 
@@ -29,6 +30,19 @@ struct RowSet {
   }
 };
 
+// Bounds checking (builds with -DHJ_CHECK_BOUNDS, libhjb200_check.so): the
+// extent of every field a stage kernel touches; each global access is tested
+// against it and violations are counted in device memory (hj_bounds_violations).
+// compute-sanitizer is closed on this pool, this is its replacement.
+struct Extent {
+  const void* lo;
+  const void* hi;
+};
+struct BoundsCheck {
+  Extent in, y0, out, mask, aux;
+  unsigned long long* oob;   // device counter; NULL in normal builds
+};
+
 struct StageArgs {
   GridArgs g;
   RowSet zr;        // axis-0 brick rows (3-D brick) / pre-pass segments (4-D) of this launch
@@ -51,7 +65,21 @@ struct StageArgs {
   hj_stats* stats;
   double* aux0;     // 4-D brick path: (p_avg0, d0) pairs per node from the axis-0 pre-pass
                     // (interleaved: one 16-B load per node in the fused walk)
+  BoundsCheck bc;
 };
+
+#ifdef HJ_CHECK_BOUNDS
+__device__ __forceinline__ void chk_extent(const BoundsCheck& b, const Extent& e, const void* p, int bytes,
+                                           const char* what, const char* file, int line) {
+  if (b.oob && (p < e.lo || (const char*)p + bytes > (const char*)e.hi)) {
+    if (atomicAdd(b.oob, 1ull) < 8)
+      printf("hj bounds: %s at %s:%d ptr %p outside [%p, %p)\n", what, file, line, p, e.lo, e.hi);
+  }
+}
+#define HJ_CHK(P, which, ptr, bytes) ::hj::chk_extent((P).bc, (P).bc.which, (const void*)(ptr), (bytes), #which, __FILE__, __LINE__)
+#else
+#define HJ_CHK(P, which, ptr, bytes) ((void)0)
+#endif
 
 // Split a linear owned-node index into (problem, per-axis indices) and the
 // element offset of that node from the problem-0 base pointer.

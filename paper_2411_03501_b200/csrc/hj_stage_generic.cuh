@@ -40,7 +40,10 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
         if (k >= 3 - W && k <= 3 + W)
+        {
+          if (inner) HJ_CHK(P, in, line + (long long)(ix[a] - 3 + k) * A.stride, 8);
           uu[a][k] = inner ? line[(long long)(ix[a] - 3 + k) * A.stride] : fetch(line, A, ix[a] - 3 + k);
+        }
         else
           uu[a][k] = 0.0;
       }
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(256) k_stage_generic(const StageArgs P) {
       out = (pv > out) ? pv : out;
     }
     if (!finite(out)) flags |= HJ_NF_OUTPUT;
+    HJ_CHK(P, out, P.y_out + off, 8);
     P.y_out[off] = out;
   }
   if (P.stats) reduce_stats<DIM>(P.stats, flags, P.tag, P.want_ranges != 0, lo, hi);
