@@ -10,6 +10,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
+import re
 import subprocess
 import sys
 
@@ -26,8 +27,21 @@ FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,
          f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
 
 
-def _deps() -> list[str]:
-    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "hjb200.h")])
+def _deps(src: str) -> list[str]:
+    """Headers a translation unit includes, transitively (quoted includes)."""
+    seen: set[str] = set()
+    todo = [src]
+    while todo:
+        f = todo.pop()
+        with open(f) as fh:
+            for line in fh:
+                m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+                if m:
+                    h = os.path.normpath(os.path.join(os.path.dirname(f), m.group(1)))
+                    if os.path.exists(h) and h not in seen:
+                        seen.add(h)
+                        todo.append(h)
+    return sorted(seen)
 
 
 def _stale(target: str, sources: list[str]) -> bool:
@@ -39,7 +53,7 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 def _compile(src: str, verbose: bool, check: bool = False) -> str:
     obj = os.path.join(OBJ + ("_check" if check else ""), os.path.basename(src)[:-3] + ".o")
-    if _stale(obj, [src, *_deps()]):
+    if _stale(obj, [src, *_deps(src)]):
         cmd = [NVCC, *ARCH, *FLAGS, *(["-DHJ_CHECK_BOUNDS"] if check else []), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -345,7 +345,8 @@ static void set_rows(StageArgs& P, int w, int part, int64_t plo = 0, int64_t phi
 
 static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
                       const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
-                      hj_stats* stats, int32_t tag, int part, int64_t plo, int64_t phi, void* stream) {
+                      hj_stats* stats, int32_t tag, int part, int64_t plo, int64_t phi, void* stream,
+                      StageArgs* build_only = nullptr) {
   const int w = ghost_width_of(scheme);
   if (w < 0) return fail(HJ_EINVAL, "unknown derivative scheme %d", scheme);
   StageArgs P;
@@ -387,6 +388,10 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
   P.y_out = y_out;
   P.mask_prev = mask_prev;
   P.stats = stats;
+  if (build_only) {   // validated arguments for a caller that launches itself (hj_integrate)
+    *build_only = P;
+    return HJ_OK;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (P.g.dim == 4) {
     // 4-D brick path: scratch for the axis-0 pre-pass (p_avg0, d0)
@@ -603,3 +608,14 @@ int hj_divided_differences(const hj_grid* g, int axis, int width, int order, con
 }
 
 }  // extern "C"
+
+namespace hj {
+// hj_stage's validation and argument build without the launch
+int stage_args(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+               const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+               hj_stats* stats, int32_t tag, StageArgs* P) {
+  return stage_impl(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, HJ_PART_ALL,
+                    0, 0, nullptr, P);
+}
+}  // namespace hj
+

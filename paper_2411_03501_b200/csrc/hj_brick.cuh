@@ -71,6 +71,10 @@ constexpr int CRD_Y = BZ, CRD_X = BZ + BYX, CRD_T0 = BZ + 2 * BYX, CRD_T1 = BZ +
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
+// UNR flags (A/B variants): the fused first-axis walk unrolled by 2; 4-D
+// pre-pass segments of 4 brick rows (32 nodes) instead of PRE_ROWS
+constexpr int UNR_Z2 = 16, UNR_PRE4 = 32;
+
 // UNR: unroll of the WENO walk (the window rotates with period 4).  The walk
 // covers the brick edge N but stops after the first nv nodes (nv < N on the
 // partial bricks of the far faces: 121 = 7*16 + 9 nodes, the 4-D grid of
@@ -220,11 +224,11 @@ template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<AO>& V, BrickSmem& S,
                                             const BrickCoord c, unsigned& flags, const BrickCoord* next,
                                             bool load) {
-  constexpr int WALK_UNROLL = UNR;   // WENO walk unroll (removes window rotation moves)
+  constexpr int WALK_UNROLL = UNR & 15;   // WENO walk unroll (removes window rotation moves)
   // the fused first-axis walk carries the whole per-node update in its body:
   // kept rolled, so the hot loops fit the instruction cache (ncu: 8 % of the
   // samples were no_instructions with both walks unrolled)
-  constexpr int ZWALK_UNROLL = HJ_ZWALK_UNROLL;
+  constexpr int ZWALK_UNROLL = (UNR & UNR_Z2) ? 2 : HJ_ZWALK_UNROLL;
   const GridArgs& G = P.g;
   const AxisView& A0 = G.ax[AO];
   const AxisView& A1 = G.ax[AO + 1];
@@ -607,34 +611,34 @@ __device__ __forceinline__ void stage_brick(const StageArgs& P, const BrickView<
 
 // ---- 4-D pre-pass: the axis-0 walks (one thread per column segment, coalesced
 // across the last axis); p_avg0 and d0 = 0 + (alpha0*0.5)*(R0-L0) to scratch.
-// A segment covers up to PRE_ROWS consecutive 8-plane rows of the launch's
-// row set (zr: rows lo..lo+split-1, then hs..): longer segments amortise the
-// walk's window fill (5 faces + 3 centres) over more nodes.
+// A segment covers up to PR consecutive 8-plane rows of the launch's row set
+// (zr: rows lo..lo+split-1, then hs..): longer segments amortise the walk's
+// window fill (5 faces + 3 centres) over more nodes.
 constexpr int PRE_ROWS = 2;
-constexpr int PRE_SEG = PRE_ROWS * SEG;   // 16 nodes
 
+template <int PR>
 __host__ __device__ __forceinline__ int pre_segments(const RowSet& r) {
-  return (r.split + PRE_ROWS - 1) / PRE_ROWS + (r.cnt - r.split + PRE_ROWS - 1) / PRE_ROWS;
+  return (r.split + PR - 1) / PR + (r.cnt - r.split + PR - 1) / PR;
 }
 
-template <int SCHEME>
+template <int SCHEME, int PR>
 __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   const GridArgs& G = P.g;
   const long long plane = G.stride[0];
   const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= plane) return;
   const RowSet& R = P.zr;
-  const int nseg = pre_segments(R);
+  const int nseg = pre_segments<PR>(R);
   const int sidx = blockIdx.y % nseg, pb = blockIdx.y / nseg;
-  const int na = (R.split + PRE_ROWS - 1) / PRE_ROWS;
+  const int na = (R.split + PR - 1) / PR;
   int row, rows;   // first row of the segment and its row count
   if (sidx < na) {
-    row = R.lo + sidx * PRE_ROWS;
-    rows = min(PRE_ROWS, R.split - sidx * PRE_ROWS);
+    row = R.lo + sidx * PR;
+    rows = min(PR, R.split - sidx * PR);
   } else {
     const int k = sidx - na;
-    row = R.hs + k * PRE_ROWS;
-    rows = min(PRE_ROWS, (R.cnt - R.split) - k * PRE_ROWS);
+    row = R.hs + k * PR;
+    rows = min(PR, (R.cnt - R.split) - k * PR);
   }
   const int z0 = row * SEG;
   const long long base = (long long)pb * G.batch_stride + pos;
@@ -642,11 +646,33 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   const AxisView A0 = G.ax[0];
   const double ah = P.alpha_half[0];
   const int zmax = min(rows * SEG, G.n[0] - z0);
-  // a segment whose stencils stay inside the owned planes loads directly
+  // a segment whose stencils stay inside the owned planes loads directly;
+  // the walk reads k = -3..2 for its window, then k = 3, 4, ... one per step:
+  // those arrive through a two-deep register queue (the load of node k+2 is
+  // issued when node k is consumed, a whole walk step before it is needed)
   const bool inner = z0 >= 3 && z0 + zmax + 3 <= G.n[0];
+  const double* cz = col + (long long)z0 * plane;
+  const int kmax = zmax + 2;   // last index the walk reads
+  double q0 = 0.0, q1 = 0.0;
+  if (inner) {
+    HJ_CHK(P, in, cz + 3 * plane, 8);
+    HJ_CHK(P, in, cz + 4 * plane, 8);
+    q0 = cz[3 * plane];
+    q1 = (4 <= kmax) ? cz[4 * plane] : 0.0;
+  }
   auto ld = [&](int k) -> double {
-    if (inner) HJ_CHK(P, in, col + (long long)(z0 + k) * plane, 8);
-    return inner ? col[(long long)(z0 + k) * plane] : fetch(col, A0, z0 + k);
+    if (!inner) return fetch(col, A0, z0 + k);
+    if (k < 3) {
+      HJ_CHK(P, in, cz + (long long)k * plane, 8);
+      return cz[(long long)k * plane];
+    }
+    const double v = q0;
+    q0 = q1;
+    if (k + 2 <= kmax) {
+      HJ_CHK(P, in, cz + (long long)(k + 2) * plane, 8);
+      q1 = cz[(long long)(k + 2) * plane];
+    }
+    return v;
   };
   auto emit = [&](int i, double L, double R2) {
     if (i < zmax) {
@@ -656,7 +682,7 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
       reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R2), 0.0 + ah * (R2 - L));
     }
   };
-  line_walk<SCHEME, 1, PRE_SEG>(ld, G.sp[0], emit, zmax);
+  line_walk<SCHEME, 1, PR * SEG>(ld, G.sp[0], emit, zmax);
 }
 
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
@@ -680,8 +706,13 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
   if (AO) {
     const long long plane = G.stride[0];
-    dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments(P.zr) * G.batch));
-    k_axis0_walk<SCHEME><<<pg, 256, 0, s>>>(P);
+    if (UNR & UNR_PRE4) {   // A/B: 32-node pre-pass segments
+      dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments<4>(P.zr) * G.batch));
+      k_axis0_walk<SCHEME, 4><<<pg, 256, 0, s>>>(P);
+    } else {
+      dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments<PRE_ROWS>(P.zr) * G.batch));
+      k_axis0_walk<SCHEME, PRE_ROWS><<<pg, 256, 0, s>>>(P);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -7,6 +7,7 @@ namespace hj {
 cudaError_t launch_brick_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
 cudaError_t launch_brick_eno(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
 cudaError_t launch_brick_weno5_fma(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
+cudaError_t launch_tile(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
 
 // HJ_STAGE_KERNEL selects the stage kernel for A/B measurements:
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
@@ -26,6 +27,8 @@ static int stage_variant() {
     if (e && std::string(e) == "brick_u2") v = 4;       // WENO5 walks unrolled by 2
     if (e && std::string(e) == "brick_noload") v = 5;   // A/B bound: tiles loaded once per CTA (wrong results)
     if (e && std::string(e) == "brick_nopf") v = 6;     // A/B: no L2 prefetch of the next brick
+    if (e && std::string(e) == "brick_x") v = 7;        // A/B slot (hj_brick_weno.cu: the variant under test)
+    if (e && std::string(e) == "tile_stages") v = 8;    // small 3-D grids: tile kernel per stage, no persistent launch
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
@@ -52,7 +55,12 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
   int dev = 0;
   cudaGetDevice(&dev);
   const int nsm = sm_count(dev);
-  if (variant != 3 && variant != 5 && nbricks < 2LL * nsm) return cudaSuccess;
+  if (variant != 3 && variant != 5 && nbricks < 2LL * nsm) {
+    // small 3-D grids: the tile kernel (one node per thread, stencils from
+    // shared memory); the per-node generic kernel for the rest
+    if ((variant == 1 || variant == 8) && P.g.dim == 3) return launch_tile(scheme, P, s, handled);
+    return cudaSuccess;
+  }
   if (variant == 6) {
     StageArgs Q = P;
     Q.no_prefetch = 1;
@@ -74,7 +82,29 @@ cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bo
 }
 }  // namespace hj
 
+namespace hj {
+// hj_integrate runs an interval's stage sequence as one persistent launch
+// (hj_stage_generic.cuh k_stage_persist) where the per-stage kernel would be
+// the generic one anyway: the default dispatch, grids below the brick
+// kernels' size (fewer bricks than 2 per SM; any 1-D/2-D grid), no range
+// statistics, at most 2^22 nodes.
+bool persist_applies(const StageArgs& P) {
+  if (stage_variant() != 1 || P.want_ranges) return false;
+  const long long total = P.g.cells * P.g.batch;
+  if (total > (1LL << 22)) return false;
+  if (P.g.dim == 3 || P.g.dim == 4) {
+    const int ao = P.g.dim - 3;
+    const long long nbricks = (long long)((P.g.n[ao + 2] + 15) / 16) * ((P.g.n[ao + 1] + 15) / 16) *
+                              ((P.g.n[ao] + 7) / 8) * (ao ? (long long)P.g.n[0] : 1) * P.g.batch;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (nbricks >= 2LL * sm_count(dev)) return false;
+  }
+  return true;
+}
+}  // namespace hj
+
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 6) return -1;
+  if (variant < -1 || variant > 8) return -1;
   return hj::set_stage_variant(variant);
 }

@@ -68,6 +68,25 @@ struct StageArgs {
   BoundsCheck bc;
 };
 
+// Stage sequence of one persistent launch (hj_integrate -> k_stage_persist,
+// hj_stage_generic.cuh)
+struct PersistStage {
+  double dt;
+  int32_t tag;
+  int8_t src, y0, dst;   // buffer ids: 0 = the initial state (read only), 1..3 = work buffers; y0 -1: none
+  int8_t kind;           // HJ_STAGE_*
+  int8_t mask;           // HJ_MASK_* applied to this stage's output
+  int8_t pad[7];
+};
+constexpr int PERSIST_MAX_STAGES = 1024;
+struct PersistArgs {
+  const double* buf[4];
+  const double* mask_prev;
+  unsigned* bar;         // grid barrier words (BAR_WORDS, hj_stage_generic.cuh), zeroed by the launcher
+  int nstages;
+  PersistStage st[PERSIST_MAX_STAGES];
+};
+
 #ifdef HJ_CHECK_BOUNDS
 __device__ __forceinline__ void chk_extent(const BoundsCheck& b, const Extent& e, const void* p, int bytes,
                                            const char* what, const char* file, int line) {

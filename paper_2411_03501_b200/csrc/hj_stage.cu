@@ -68,6 +68,39 @@ cudaError_t launch_stage_generic(int scheme, const StageArgs& P, cudaStream_t s)
   }
 }
 
+cudaError_t launch_persist_adv(int scheme, const StageArgs& P, const PersistArgs& A, cudaStream_t s);
+cudaError_t launch_persist_rockets(int scheme, const StageArgs& P, const PersistArgs& A, cudaStream_t s);
+cudaError_t launch_persist_air3d(int scheme, const StageArgs& P, const PersistArgs& A, cudaStream_t s);
+cudaError_t launch_persist_di4(int scheme, const StageArgs& P, const PersistArgs& A, cudaStream_t s);
+
+cudaError_t launch_persist(int scheme, const StageArgs& P, const PersistArgs& A, cudaStream_t s) {
+  switch (P.ham.kind) {
+    case HJ_HAM_ADVECTION: return launch_persist_adv(scheme, P, A, s);
+    case HJ_HAM_ROCKETS:
+    case HJ_HAM_ROCKETS_EXTREMAL: return launch_persist_rockets(scheme, P, A, s);
+    case HJ_HAM_AIR3D: return launch_persist_air3d(scheme, P, A, s);
+    default: return launch_persist_di4(scheme, P, A, s);
+  }
+}
+
+cudaError_t launch_tile_adv(int scheme, const StageArgs& P, cudaStream_t s);
+cudaError_t launch_tile_rockets(int scheme, const StageArgs& P, cudaStream_t s);
+cudaError_t launch_tile_air3d(int scheme, const StageArgs& P, cudaStream_t s);
+
+// small 3-D grids: the tile kernel (hj_tile.cuh); *handled = false for a
+// Hamiltonian without a 3-D tile instantiation
+cudaError_t launch_tile(int scheme, const StageArgs& P, cudaStream_t s, bool* handled) {
+  *handled = P.g.dim == 3;
+  if (!*handled) return cudaSuccess;
+  switch (P.ham.kind) {
+    case HJ_HAM_ADVECTION: return launch_tile_adv(scheme, P, s);
+    case HJ_HAM_ROCKETS:
+    case HJ_HAM_ROCKETS_EXTREMAL: return launch_tile_rockets(scheme, P, s);
+    case HJ_HAM_AIR3D: return launch_tile_air3d(scheme, P, s);
+    default: *handled = false; return cudaSuccess;
+  }
+}
+
 cudaError_t launch_derivs(int scheme, const GridArgs& G, int axis, int eps_mode, const double* v,
                           double* left, double* right, cudaStream_t s) {
   const long long total = G.cells * G.batch;

@@ -25,7 +25,9 @@ def require():
 
 STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always": 3, "brick_u2": 4,
                  "brick_noload": 5,   # brick_noload: A/B timing bound only, results are wrong
-                 "brick_nopf": 6}     # no L2 prefetch of the next brick (A/B)
+                 "brick_nopf": 6,     # no L2 prefetch of the next brick (A/B)
+                 "brick_x": 7,        # A/B slot: the variant under test (hj_brick_weno.cu)
+                 "tile_stages": 8}    # small 3-D grids: the tile kernel launched per stage (no persistent launch)
 
 
 def set_stage_kernel(name: str) -> str:

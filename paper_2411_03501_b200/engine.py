@@ -183,6 +183,14 @@ class FusedIntegrator:
     pipeline_first = 16              # planes of the first H2D chunk
     pipeline_drain = 16              # planes per stage launch once the whole input has arrived
 
+    pipeline_ramp = 0                # row-sized H2D chunks after the first
+    pipeline_tail = 0                # last planes delivered in row-sized H2D chunks
+
+    def _plan(self, n0: int, stages: int):
+        return pipeline_plan(n0, stages, int(self.pipeline_chunk), first=int(self.pipeline_first),
+                             drain=int(self.pipeline_drain), ramp=int(self.pipeline_ramp),
+                             tail=int(self.pipeline_tail))
+
     def _pipeline_ok(self, opts, y_host: np.ndarray) -> bool:
         # (a periodic first axis wraps the stencil of the first planes onto the
         # last ones, which arrive last: no pipeline)
@@ -245,8 +253,7 @@ class FusedIntegrator:
         # the stage before it (or the latest input chunk), so launches of
         # different stages overlap and fill each other's partial last waves
         last_ev = [None] * (len(kinds) + 1)          # [0]: input chunks, [k+1]: stage k's latest launch
-        for op, k, lo, hi in pipeline_plan(n0, len(kinds), int(self.pipeline_chunk),
-                                          first=int(self.pipeline_first), drain=int(self.pipeline_drain)):
+        for op, k, lo, hi in self._plan(n0, len(kinds)):
             if op == "h2d":
                 if staged is not None:
                     for f in staged.pop(lo):
@@ -290,8 +297,7 @@ class FusedIntegrator:
         dst, srcn = self._staging.numpy(), src.numpy()
         n0 = src.shape[0]
         out: dict[int, list] = {}
-        for op, _, lo, hi in pipeline_plan(n0, 1, int(self.pipeline_chunk), first=int(self.pipeline_first),
-                                          drain=int(self.pipeline_drain)):
+        for op, _, lo, hi in self._plan(n0, 1):
             if op != "h2d":
                 continue
             step = max(1, -(-(hi - lo) // int(self.staging_threads)))
@@ -411,10 +417,13 @@ class FusedIntegrator:
 
 
 def pipeline_plan(n0: int, stages: int, chunk: int, reach: int = 3, row: int = 8, first: int = 16,
-                  drain: int = 16) -> list[tuple[str, int, int, int]]:
+                  drain: int = 16, ramp: int = 0, tail: int = 0) -> list[tuple[str, int, int, int]]:
     """Schedule of the pipelined host->host step over axis-0 planes [0, n0):
-    ("h2d", -1, lo, hi) input chunks (a short first chunk, then ``chunk``
-    planes), ("stage", k, lo, hi) launches of stage k over planes whose
+    ("h2d", -1, lo, hi) input chunks -- a first chunk of ``first`` planes,
+    ``ramp`` chunks of ``row`` planes, ``chunk``-plane chunks, and the last
+    ``tail`` planes again in ``row``-plane chunks (short chunks at both ends
+    start the first output copy early and leave little work behind the last
+    input copy) -- ("stage", k, lo, hi) launches of stage k over planes whose
     stencil inputs are complete -- ``reach`` planes behind the previous
     stage's front (or its end), rounded down to the kernels' ``row``-plane
     rows -- and ("d2h", -1, lo, hi) copies of the last stage's finished
@@ -422,10 +431,17 @@ def pipeline_plan(n0: int, stages: int, chunk: int, reach: int = 3, row: int = 8
     ``drain`` planes per round, so the final copies start early.  Pure host
     logic (tests/test_host_logic.py checks coverage and dependencies)."""
     chunk = max(row, (chunk // row) * row)
-    first = min(chunk, first)
-    bounds = [min(first, n0)] + list(range(first + chunk, n0, chunk))
-    if bounds[-1] != n0:
-        bounds.append(n0)
+    drain = max(row, (drain // row) * row)
+    first = max(1, min(first, n0))
+    bounds = [first]
+    for _ in range(ramp):
+        if bounds[-1] < n0:
+            bounds.append(min(n0, bounds[-1] + row))
+    body_end = max(bounds[-1], n0 - max(0, tail))
+    while bounds[-1] + chunk < body_end:
+        bounds.append(bounds[-1] + chunk)
+    while bounds[-1] < n0:
+        bounds.append(min(n0, bounds[-1] + (row if bounds[-1] >= body_end else body_end - bounds[-1])))
     plan: list[tuple[str, int, int, int]] = []
     done = [0] * stages
     arrived, nxt = 0, 0

@@ -46,6 +46,7 @@ def main():
     dt = 0.5 / float(np.sum(cfg.partials.alphas(0.0, g) / g.spacings))
     cells = y0.numel()
     out = {}
+    ref = None
     for v in variants:
         old = dev.set_stage_kernel(v)
         fi = FusedIntegrator(g, cfg, dg=dg)
@@ -65,6 +66,11 @@ def main():
         stage = [a.elapsed_time(b) for a, b in ev]
         out[v] = {"ms_per_rk3_step": ms, "cell_updates_per_s": cells * 3 / (ms / 1e3),
                   "stage_ms": [float(np.mean(stage[k::3])) for k in range(3)]}
+        # bitwise against the first variant after the same 23 steps (timing-only variants differ)
+        if ref is None:
+            ref = y.clone()
+        else:
+            out[v]["bitwise_vs_" + variants[0]] = bool(torch.equal(y, ref))
         dev.set_stage_kernel(old)
         del fi, y
     print(json.dumps({"config": cfgname, "grid": list(g.counts), "results": out}), flush=True)

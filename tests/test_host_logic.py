@@ -179,10 +179,12 @@ def test_reference_names_exported():
 @pytest.mark.parametrize("n0", [16, 17, 40, 61, 301, 801])
 @pytest.mark.parametrize("stages", [1, 2, 3])
 @pytest.mark.parametrize("chunk", [8, 16, 32, 48, 64])
-def test_pipeline_plan_covers_and_respects_dependencies(n0, stages, chunk):
+@pytest.mark.parametrize("shape", [(16, 0, 0, 16), (11, 2, 24, 8), (5, 1, 100, 4), (40, 3, 8, 24)])
+def test_pipeline_plan_covers_and_respects_dependencies(n0, stages, chunk, shape):
     from paper_2411_03501_b200.engine import pipeline_plan
 
-    plan = pipeline_plan(n0, stages, chunk)
+    first, ramp, tail, drain = shape
+    plan = pipeline_plan(n0, stages, chunk, first=first, ramp=ramp, tail=tail, drain=drain)
     arrived = 0
     done = [0] * stages
     copied = 0
