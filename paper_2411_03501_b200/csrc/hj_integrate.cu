@@ -126,6 +126,11 @@ int run_persistent(const hj_grid* g, int scheme, const hj_ham* ham, const double
     }
     cudaError_t e = cudaMemsetAsync(bar, 0, BAR_WORDS * sizeof(unsigned), s);
     if (e == cudaSuccess) e = launch_persist(scheme, P, *X, s);
+    if (e != cudaSuccess && base == 0 && e != cudaErrorIllegalAddress && e != cudaErrorLaunchFailure) {
+      // the cooperative launch itself was refused (nothing ran): per-stage launches instead
+      cudaGetLastError();
+      return NOT_PERSISTENT;
+    }
     if (e != cudaSuccess) {
       std::string msg = std::string("hj_integrate (persistent): ") + cudaGetErrorString(e);
       rc = set_error(HJ_ECUDA, msg.c_str());
