@@ -222,6 +222,9 @@ int hj_eval_hamiltonian(const hj_grid* g, const hj_ham* ham, const double* const
  * dt = cfl*bound, min(max_step) (max_step <= 0: none), clipped to the span,
  * t = t1 on the last step; each TVD-RK stage one hj_stage launch (tags
  * step*4 + stage), the mask applied in the final stage; no device sync.
+ * Small grids (where hj_stage would pick the per-node / tile kernel) run the
+ * whole stage schedule as one cooperative launch per 1024 stages with a grid
+ * barrier between stages -- the same node updates, bit for bit.
  * y_init is not written; buf0..2 are the work buffers (one of them, or
  * y_init when no step is taken, is returned in *y_final).
  * info (host, 6 doubles): t_final, steps, min_dt, max_dt, bad_dt_flag, bad_dt. */

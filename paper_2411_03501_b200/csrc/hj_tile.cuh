@@ -68,10 +68,20 @@ __device__ __forceinline__ void tile_stage(const StageArgs& P, const StageIO& io
                        (2 * TLH * TLZ * TLY + TL_THREADS - 1) / TL_THREADS;
   const double* srcs[NPUT];   // slot k: the load of the k-th position (nullptr: none / ghost)
   int dsts[NPUT];
+  // a tile whose stencils stay inside the domain (most of them) takes every
+  // position from memory without the per-position domain tests
+  const bool interior = x0 >= W && x0 + TLX + W <= n2 && y0 >= W && y0 + TLY + W <= n1 && z0 >= W &&
+                        z0 + TLZ + W <= n0;
   auto put = [&](int k, int lz, int ly, int lx) {
     const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-    const bool ix = gx >= 0 && gx < n2, iy = gy >= 0 && gy < n1, iz = gz >= 0 && gz < n0;
     const int di = ((lz + TLH) * TBY + (ly + TLH)) * TBX + (lx + TLH);
+    if (interior) {
+      srcs[k] = vin + (gz * s0 + gy * s1 + gx);
+      HJ_CHK(P, in, srcs[k], 8);
+      dsts[k] = di;
+      return;
+    }
+    const bool ix = gx >= 0 && gx < n2, iy = gy >= 0 && gy < n1, iz = gz >= 0 && gz < n0;
     if (ix && iy && iz) {
       srcs[k] = vin + (gz * s0 + gy * s1 + gx);
       HJ_CHK(P, in, srcs[k], 8);
@@ -161,20 +171,18 @@ __device__ __forceinline__ void tile_stage(const StageArgs& P, const StageIO& io
   }
   double pbar[3];
   double diss = 0.0;
+  unsigned big = 0u;   // largest exponent field of the node's checked values (finite <=> < 0x7FF00000)
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const LR lr = lrs[a];
-    if (!finite(lr.l) || !finite(lr.r)) flags |= HJ_NF_DERIV;
+    big = max(big, max(abs_hi(lr.l), abs_hi(lr.r)));
     pbar[a] = 0.5 * (lr.l + lr.r);                        // term.py:101
     diss = diss + P.alpha_half[a] * (lr.r - lr.l);        // term.py:84-86
   }
   const double H = hamiltonian<HAM, 3>(P.ham, G.nodes, ixs, pbar);
-  if (!finite(H)) flags |= HJ_NF_HAM;
   if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
   const double delta = diss - H;                          // term.py:113
-  if (!finite(delta)) flags |= HJ_NF_DELTA;
   const double y = c[0];
-  if (!finite(y)) flags |= HJ_NF_INPUT;
   const long long off = b * G.batch_stride + ixs[0] * s0 + ixs[1] * s1 + ixs[2];
   const double yz = (io.stage >= HJ_STAGE_RK2_AVG) ? ldf<CG>(io.y0 + off) : 0.0;
   double out = stage_update(io.stage, io.dt, y, yz, delta);
@@ -185,7 +193,16 @@ __device__ __forceinline__ void tile_stage(const StageArgs& P, const StageIO& io
     const double pv = ldf<CG>(io.mask_prev + off);
     out = (pv > out) ? pv : out;
   }
-  if (!finite(out)) flags |= HJ_NF_OUTPUT;
+  big = max(max(big, abs_hi(H)), max(max(abs_hi(delta), abs_hi(y)), abs_hi(out)));
+  if (big >= 0x7FF00000u) {   // rare: the per-class flags (one compare on the common path)
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (!finite(lrs[a].l) || !finite(lrs[a].r)) flags |= HJ_NF_DERIV;
+    if (!finite(H)) flags |= HJ_NF_HAM;
+    if (!finite(delta)) flags |= HJ_NF_DELTA;
+    if (!finite(y)) flags |= HJ_NF_INPUT;
+    if (!finite(out)) flags |= HJ_NF_OUTPUT;
+  }
   HJ_CHK(P, out, io.y_out + off, 8);
   io.y_out[off] = out;
 }

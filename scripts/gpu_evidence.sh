@@ -3,7 +3,7 @@
 #  (profiles/fp64_ops.json, traffic.json, copied to gpurun_out/); the bench
 #  line of every config; the reference arm of every config; launch lists.
 TAG=${1:-ev}
-timeout 2400 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/${TAG}_gputests.log 2>&1; echo "rc $?" >> gpurun_out/${TAG}_gputests.log
+[ -n "$SKIP_TESTS" ] || timeout 2400 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/${TAG}_gputests.log 2>&1; echo "rc $?" >> gpurun_out/${TAG}_gputests.log
 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 rm -f profiles/fp64_ops.json profiles/traffic.json
 for spec in c2:weno5:27270901 c4:weno5:214358881 c5:weno5:8242408 c2:weno5_fma:27270901; do
@@ -13,11 +13,17 @@ for spec in c2:weno5:27270901 c4:weno5:214358881 c5:weno5:8242408 c2:weno5_fma:2
       -o gpurun_out/${TAG}_prof_${cfg}_$sch python scripts/variant_probe.py $cfg auto > gpurun_out/${TAG}_ncu_${cfg}_$sch.log 2>&1 && \
   python scripts/ncu_summary.py gpurun_out/${TAG}_prof_${cfg}_$sch.ncu-rep $nodes --stamp ${cfg}_$sch --traffic ${cfg}_${sch}_1 \
       > gpurun_out/${TAG}_ncu_${cfg}_$sch.json 2>&1
+  # per-instruction source page (scripts/sass_regions.py), then drop the report
+  # (gpurun copies back at most 64 MiB of gpurun_out/)
+  ncu -i gpurun_out/${TAG}_prof_${cfg}_$sch.ncu-rep --page source --csv --print-source sass \
+      > gpurun_out/${TAG}_src_${cfg}_$sch.csv 2>/dev/null && gzip -f gpurun_out/${TAG}_src_${cfg}_$sch.csv
+  rm -f gpurun_out/${TAG}_prof_${cfg}_$sch.ncu-rep
 done
 # C1: the persistent tile kernel (one launch = one interval of 158 ENO2/RK2 stages of 93636 nodes)
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tile_persist -s 2 -c 1 \
     -o gpurun_out/${TAG}_prof_c1_eno2 python scripts/c1_persist_probe.py auto > gpurun_out/${TAG}_ncu_c1_eno2.log 2>&1 && \
 python scripts/ncu_summary.py gpurun_out/${TAG}_prof_c1_eno2.ncu-rep 14794488 > gpurun_out/${TAG}_ncu_c1_eno2.json 2>&1
+rm -f gpurun_out/${TAG}_prof_c1_eno2.ncu-rep
 cp profiles/fp64_ops.json gpurun_out/${TAG}_fp64_ops.json; cp profiles/traffic.json gpurun_out/${TAG}_traffic.json
 for cfg in c2 c1 c3 c4 c5; do timeout 900 python bench.py --config $cfg > gpurun_out/${TAG}_bench_$cfg.log 2>&1; done
 for cfg in c2 c1 c3 c4 c5; do timeout 900 python bench.py --impl reference --config $cfg > gpurun_out/${TAG}_bench_ref_$cfg.log 2>&1; done

@@ -29,11 +29,12 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
-@pytest.fixture(params=["auto", "brick_always", "generic"])
+@pytest.fixture(params=["auto", "brick_always", "generic", "tile_stages"])
 def stage_kernel(request):
     """Run a GPU parity test under every fused-stage kernel family: the
-    default dispatch, the brick kernels forced even on tiny grids, and the
-    per-node generic kernel."""
+    default dispatch (small grids: the tile kernel, an integration interval
+    in one persistent launch), the brick kernels forced even on tiny grids,
+    the per-node generic kernel, and the tile kernel launched per stage."""
     from paper_2411_03501_b200 import device as dev
 
     old = dev.set_stage_kernel(request.param)
