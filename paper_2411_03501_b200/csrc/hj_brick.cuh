@@ -71,9 +71,10 @@ constexpr int CRD_Y = BZ, CRD_X = BZ + BYX, CRD_T0 = BZ + 2 * BYX, CRD_T1 = BZ +
 // LDS/STS conflict-free whether the lanes of a warp vary x or y
 __device__ __forceinline__ int swz(int z, int y, int x) { return (z * BYX + y) * BYX + (x ^ y); }
 
-// UNR flags (A/B variants): the fused first-axis walk unrolled by 2; 4-D
-// pre-pass segments of 4 brick rows (32 nodes) instead of PRE_ROWS
-constexpr int UNR_Z2 = 16, UNR_PRE4 = 32;
+// UNR flags (A/B variants): the fused first-axis walk unrolled by 2; the 4-D
+// pre-pass reading its columns from global memory through a register queue
+// (32-node segments) instead of staging them in shared memory
+constexpr int UNR_Z2 = 16, UNR_PREREG = 32;
 
 // UNR: unroll of the WENO walk (the window rotates with period 4).  The walk
 // covers the brick edge N but stops after the first nv nodes (nv < N on the
@@ -685,6 +686,69 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   line_walk<SCHEME, 1, PR * SEG>(ld, G.sp[0], emit, zmax);
 }
 
+// The same pre-pass with the CTA's 256 column segments staged in shared
+// memory first: rows k = -3 .. zmax+2 of the segment (at most 22), 256
+// consecutive plane positions each, all in flight at once (cp.async for
+// segments inside the owned planes, fetch() ghosts otherwise); every thread
+// then walks its column from shared memory.  The global-load version above
+// waits on one dependent load per walk step (long_scoreboard 35 % of its
+// stall samples in r01).
+constexpr int PRE_SROWS = PRE_ROWS * SEG + 6;   // 22
+
+template <int SCHEME>
+__global__ void __launch_bounds__(256, 2) k_axis0_walk_smem(const StageArgs P) {
+  __shared__ double col_s[PRE_SROWS * 256];
+  const GridArgs& G = P.g;
+  const long long plane = G.stride[0];
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool on = pos < plane;
+  const RowSet& R = P.zr;
+  const int nseg = pre_segments<PRE_ROWS>(R);
+  const int sidx = blockIdx.y % nseg, pb = blockIdx.y / nseg;
+  const int na = (R.split + PRE_ROWS - 1) / PRE_ROWS;
+  int row, rows;
+  if (sidx < na) {
+    row = R.lo + sidx * PRE_ROWS;
+    rows = min(PRE_ROWS, R.split - sidx * PRE_ROWS);
+  } else {
+    const int k = sidx - na;
+    row = R.hs + k * PRE_ROWS;
+    rows = min(PRE_ROWS, (R.cnt - R.split) - k * PRE_ROWS);
+  }
+  const int z0 = row * SEG;
+  const long long base = (long long)pb * G.batch_stride + pos;
+  const double* col = P.y_in + base;
+  const AxisView A0 = G.ax[0];
+  const double ah = P.alpha_half[0];
+  const int zmax = min(rows * SEG, G.n[0] - z0);
+  const bool inner = z0 >= 3 && z0 + zmax + 3 <= G.n[0];   // CTA-uniform
+  const int t = threadIdx.x;
+  if (on) {
+    for (int k = -3; k < zmax + 3; ++k) {
+      double* dst = &col_s[(k + 3) * 256 + t];
+      if (inner) {
+        HJ_CHK(P, in, col + (long long)(z0 + k) * plane, 8);
+        cp_async8(dst, col + (long long)(z0 + k) * plane);
+      } else {
+        *dst = fetch(col, A0, z0 + k);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (!on) return;
+  auto ld = [&](int k) -> double { return col_s[(k + 3) * 256 + t]; };
+  auto emit = [&](int i, double L, double R2) {
+    if (i < zmax) {
+      const long long o = base + (long long)(z0 + i) * plane;
+      // (p_avg0, d0): term.py:101, and the dissipation sum's first term (term.py:84-86)
+      HJ_CHK(P, aux, reinterpret_cast<double2*>(P.aux0) + o, 16);
+      reinterpret_cast<double2*>(P.aux0)[o] = make_double2(0.5 * (L + R2), 0.0 + ah * (R2 - L));
+    }
+  };
+  line_walk<SCHEME, 1, PRE_ROWS * SEG>(ld, G.sp[0], emit, zmax);
+}
+
 template <int SCHEME, int HAM, int MINB, int AO, int UNR>
 static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const size_t smem = sizeof(BrickSmem);
@@ -706,12 +770,12 @@ static cudaError_t launch_brick(const StageArgs& P, cudaStream_t s) {
   const long long ctas = nbricks < (long long)MINB * nsm ? nbricks : (long long)MINB * nsm;
   if (AO) {
     const long long plane = G.stride[0];
-    if (UNR & UNR_PRE4) {   // A/B: 32-node pre-pass segments
+    if (UNR & UNR_PREREG) {   // A/B: columns from global memory, 32-node segments
       dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments<4>(P.zr) * G.batch));
       k_axis0_walk<SCHEME, 4><<<pg, 256, 0, s>>>(P);
     } else {
       dim3 pg((unsigned)((plane + 255) / 256), (unsigned)(pre_segments<PRE_ROWS>(P.zr) * G.batch));
-      k_axis0_walk<SCHEME, PRE_ROWS><<<pg, 256, 0, s>>>(P);
+      k_axis0_walk_smem<SCHEME><<<pg, 256, 0, s>>>(P);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -163,7 +163,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
       }
     }
     if (!released) {
+      unsigned spins = 0;
       while (*(volatile unsigned*)&bar[0] == gen) {
+        // ~2^28 polls (seconds): a scheduling bug ends the launch with an error instead of hanging
+        if (++spins > (1u << 28)) asm volatile("trap;");
       }
     }
     __threadfence();
