@@ -208,12 +208,25 @@ def sass_hash(symbol: str) -> str | None:
     return h.hexdigest() if n > 100 else None
 
 
-def brick_symbol(frag: str) -> str:
-    """'k_stage_brickILi3ELi3ELi2ELi0ELi2EE' -> the kernel's mangled symbol
-    (k_stage_brick(StageArgs, int); k_stage_generic(StageArgs))"""
-    base = frag.split("I", 1)[0]
-    args = "NS_9StageArgsEi" if base == "k_stage_brick" else "NS_9StageArgsE"
-    return f"_ZN2hj{len(base)}{frag}Ev{args}"
+_PARAMS = {"(StageArgs, int)": "NS_9StageArgsEi", "(StageArgs)": "NS_9StageArgsE",
+           "(StageArgs, AxesScratch)": "NS_9StageArgsENS_11AxesScratchE",
+           "(StageArgs, PersistArgs)": "NS_9StageArgsENS_11PersistArgsE"}
+
+
+def kernel_symbol(kernel: str) -> str:
+    """'void k_axis_col<3, 4, 4, 0>(StageArgs, AxesScratch)' (ncu's name) ->
+    '_ZN2hj10k_axis_colILi3ELi4ELi4ELi0EEEvNS_9StageArgsENS_11AxesScratchE'"""
+    import re
+
+    m = re.search(r"(\w+)<([^>]*)>(\(.*\))", kernel)
+    if m:
+        base, targs, params = m.group(1), [a.strip() for a in m.group(2).split(",")], m.group(3)
+        frag = base + "I" + "".join(f"Li{a}E" for a in targs) + "E"
+    else:
+        m = re.search(r"(\w+)(\(.*\))", kernel)
+        base, params, frag = m.group(1), m.group(2), m.group(1)
+    params = params.replace("hj::", "")
+    return f"_ZN2hj{len(base)}{frag}Ev{_PARAMS.get(params, 'NS_9StageArgsE')}"
 
 
 def fp64_ops(key: str):
@@ -230,9 +243,11 @@ def fp64_ops(key: str):
         ent = d.get("c2_" + key[3:])   # C3 runs the C2 kernel (same instantiation; the SASS hash is checked)
     if not isinstance(ent, dict):
         return None, f"no entry {key}"
-    now = sass_hash(ent.get("symbol", ""))
-    if now is None or now != ent.get("sass_sha256"):
-        return None, f"stale: SASS of {ent.get('kernel')} changed since the ncu count ({ent.get('source')})"
+    # one kernel per stage (brick) or the stage's kernel sequence (per-axis walk pipeline)
+    for k in ent.get("kernels", [ent]):
+        now = sass_hash(k.get("symbol", ""))
+        if now is None or now != k.get("sass_sha256"):
+            return None, f"stale: SASS of {k.get('kernel')} changed since the ncu count ({ent.get('source')})"
     return float(ent["ops_per_node"]), ent.get("source")
 
 

@@ -59,6 +59,7 @@ static int fail(int code, const char* fmt, ...) {
 }
 
 namespace hj {
+bool axes_applies(int scheme, const StageArgs& P);   // hj_fast.cu
 // for the other translation units of the library (hj_dd.cu): set the
 // thread-local message / count launches made outside this file
 int set_error(int code, const char* msg) {
@@ -393,9 +394,13 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
     return HJ_OK;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (P.g.dim == 4) {
+  const size_t span = (size_t)(P.g.batch_stride * (P.g.batch - 1) + P.g.cells);
+  const bool axes = axes_applies(scheme, P);
+  if (axes) {
+    // per-axis walk pipeline (hj_axes.cuh): dim + 1 field-sized scratch arrays
+    P.aux0 = scratch_for(s, (size_t)(P.g.dim + 1) * span);
+  } else if (P.g.dim == 4) {
     // 4-D brick path: scratch for the axis-0 pre-pass (p_avg0, d0)
-    const size_t span = (size_t)(P.g.batch_stride * (P.g.batch - 1) + P.g.cells);
     double* scratch = scratch_for(s, 2 * span);
     if (scratch) {
       P.aux0 = scratch;   // span (p_avg0, d0) pairs
@@ -405,7 +410,9 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
   bool handled = false;
   cudaError_t e = launch_stage_fast(scheme, P, s, &handled);
   if (!handled) e = launch_stage_generic(scheme, P, s);
-  return cuda_status(e, "hj_stage");
+  // kernels launched: one per axis (per-axis walk pipeline), pre-pass + brick (4-D bricks), else one
+  const uint64_t nl = (handled && axes && P.aux0) ? (uint64_t)P.g.dim : (handled && P.g.dim == 4 && P.aux0) ? 2 : 1;
+  return cuda_status(e, "hj_stage", nl);
 }
 
 int hj_stage_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,

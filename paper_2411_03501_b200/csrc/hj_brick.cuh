@@ -686,6 +686,49 @@ __global__ void __launch_bounds__(256) k_axis0_walk(const StageArgs P) {
   line_walk<SCHEME, 1, PR * SEG>(ld, G.sp[0], emit, zmax);
 }
 
+// Stage positions k = -3 .. zmax+2 (relative to node z0) of one line of axis
+// view A starting at `line` into dst[(k + 3) * pitch].  Every value that lives
+// in memory (in-domain nodes, a periodic axis' wrapped images) goes through
+// cp.async -- all in flight, nothing waits per position; dirichlet ghosts are
+// the constant; extrapolated ghosts are marked and synthesised by
+// ghost_fill() once the copies have landed (they need the edge nodes).  Same
+// values as fetch() (grid.py:203-225), bit for bit.
+__device__ __forceinline__ void stage_line(const double* line, const AxisView& A, int z0, int zmax, double* dst,
+                                           int pitch) {
+  for (int k = -3; k < zmax + 3; ++k) {
+    const int e = z0 + k;
+    double* d = dst + (k + 3) * pitch;
+    if (e >= 0 && e < A.n) {
+      cp_async8(d, line + (long long)e * A.stride);
+    } else if ((e < 0 && A.halo_lo) || (e >= A.n && A.halo_hi)) {
+      // exchanged halo planes (multi-GPU slabs); beyond them nothing in the domain reads
+      const bool in_halo = e < 0 ? e >= -A.halo_n : e < A.n + A.halo_n;
+      if (in_halo) cp_async8(d, line + (long long)e * A.stride);
+      else *d = 0.0;
+    } else if (A.bc == HJ_BC_PERIODIC) {
+      const int j = e < 0 ? ((e % A.n) + A.n) % A.n : e % A.n;
+      cp_async8(d, line + (long long)j * A.stride);
+    } else if (A.bc == HJ_BC_DIRICHLET) {
+      *d = A.bcv;
+    }
+  }
+}
+
+// The extrapolated ghosts of a line staged by stage_line (after the copies
+// of this thread -- or, for cooperative staging, of the CTA -- have landed).
+__device__ __forceinline__ void ghost_fill(const AxisView& A, int z0, int zmax, double* dst, int pitch) {
+  if (A.bc != HJ_BC_EXTRAPOLATE) return;
+  if (z0 < 3 && !A.halo_lo) {
+    const double v0 = dst[(0 - z0 + 3) * pitch], v1 = dst[(1 - z0 + 3) * pitch];
+    for (int e = z0 - 3; e < 0; ++e) dst[(e - z0 + 3) * pitch] = v0 + (double)(-e) * (v0 - v1);   // grid.py:220,222
+  }
+  if (z0 + zmax + 3 > A.n && !A.halo_hi) {
+    const double vn = dst[(A.n - 1 - z0 + 3) * pitch], vm = dst[(A.n - 2 - z0 + 3) * pitch];
+    for (int e = A.n; e < z0 + zmax + 3; ++e)
+      dst[(e - z0 + 3) * pitch] = vn + (double)(e - A.n + 1) * (vn - vm);                           // grid.py:221,223
+  }
+}
+
 // The same pre-pass with the CTA's 256 column segments staged in shared
 // memory first: rows k = -3 .. zmax+2 of the segment (at most 22), 256
 // consecutive plane positions each, all in flight at once (cp.async for
@@ -724,17 +767,17 @@ __global__ void __launch_bounds__(256, 2) k_axis0_walk_smem(const StageArgs P) {
   const bool inner = z0 >= 3 && z0 + zmax + 3 <= G.n[0];   // CTA-uniform
   const int t = threadIdx.x;
   if (on) {
-    for (int k = -3; k < zmax + 3; ++k) {
-      double* dst = &col_s[(k + 3) * 256 + t];
-      if (inner) {
+    if (inner) {
+      for (int k = -3; k < zmax + 3; ++k) {
         HJ_CHK(P, in, col + (long long)(z0 + k) * plane, 8);
-        cp_async8(dst, col + (long long)(z0 + k) * plane);
-      } else {
-        *dst = fetch(col, A0, z0 + k);
+        cp_async8(&col_s[(k + 3) * 256 + t], col + (long long)(z0 + k) * plane);
       }
+    } else {
+      stage_line(col, A0, z0, zmax, col_s + t, 256);   // (ghosts without waiting per position)
     }
   }
   cp_async_wait_all();
+  if (on && !inner) ghost_fill(A0, z0, zmax, col_s + t, 256);
   __syncthreads();
   if (!on) return;
   auto ld = [&](int k) -> double { return col_s[(k + 3) * 256 + t]; };

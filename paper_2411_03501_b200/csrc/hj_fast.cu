@@ -8,6 +8,7 @@ cudaError_t launch_brick_weno5(const StageArgs& P, cudaStream_t s, bool* handled
 cudaError_t launch_brick_eno(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
 cudaError_t launch_brick_weno5_fma(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
 cudaError_t launch_tile(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
+cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled);
 
 // HJ_STAGE_KERNEL selects the stage kernel for A/B measurements:
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
@@ -29,6 +30,7 @@ static int stage_variant() {
     if (e && std::string(e) == "brick_nopf") v = 6;     // A/B: no L2 prefetch of the next brick
     if (e && std::string(e) == "brick_x") v = 7;        // A/B slot (hj_brick_weno.cu: the variant under test)
     if (e && std::string(e) == "tile_stages") v = 8;    // small 3-D grids: tile kernel per stage, no persistent launch
+    if (e && std::string(e) == "axes") v = 9;           // brick-sized WENO5 grids: the per-axis walk pipeline
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
@@ -43,9 +45,39 @@ int set_stage_variant(int v) {
 
 // The brick kernels cover 3-D stages without range statistics whose grid
 // fits the launch geometry; everything else runs the generic per-node kernel.
+// The per-axis walk pipeline (hj_axes.cuh) covers whole-grid WENO5 launches
+// of 3-D / 4-D grids (no exchanged halos, contiguous batches, no range
+// statistics) -- by default those of brick size (measured faster than the
+// brick kernels at 301^3, 121^4 and 8 x 101^3: DESIGN.md); "axes" forces it
+// on every size (tests).  It needs (dim + 1) field-sized scratch arrays.
+bool axes_applies(int scheme, const StageArgs& P) {
+  const int v = stage_variant();
+  if ((v != 1 && v != 9) || scheme != HJ_WENO5) return false;
+  if ((P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return false;
+  if (P.g.ax[0].halo_lo || P.g.ax[0].halo_hi) return false;
+  if (P.zp.lo != 0 || P.zp.cnt != P.g.n[0]) return false;
+  if (P.g.batch > 1 && P.g.batch_stride != P.g.cells) return false;
+  bool ham_ok = false;
+  switch (P.ham.kind) {
+    case HJ_HAM_ADVECTION: ham_ok = true; break;
+    case HJ_HAM_AIR3D: case HJ_HAM_ROCKETS: case HJ_HAM_ROCKETS_EXTREMAL: ham_ok = P.g.dim == 3; break;
+    case HJ_HAM_DI4: ham_ok = P.g.dim == 4; break;
+    default: ham_ok = false;
+  }
+  if (!ham_ok) return false;
+  if (v == 9) return true;
+  const int ao = P.g.dim - 3;   // default: where the brick kernels would run
+  const long long nbricks = (long long)((P.g.n[ao + 2] + 15) / 16) * ((P.g.n[ao + 1] + 15) / 16) *
+                            ((P.g.n[ao] + 7) / 8) * (ao ? (long long)P.g.n[0] : 1) * P.g.batch;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return nbricks >= 2LL * sm_count(dev);
+}
+
 cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = false;
   const int variant = stage_variant();
+  if (P.aux0 && axes_applies(scheme, P)) return launch_axes_weno5(P, s, handled);
   if (variant == 0 || (P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return cudaSuccess;
   // too few bricks to occupy the SMs (small grids such as C1's 51x51x36):
   // the per-node kernel exposes more parallelism
@@ -105,6 +137,6 @@ bool persist_applies(const StageArgs& P) {
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 8) return -1;
+  if (variant < -1 || variant > 9) return -1;
   return hj::set_stage_variant(variant);
 }

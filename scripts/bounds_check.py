@@ -33,7 +33,7 @@ def step3(g, cfg, y, dg=None):
 
 
 def cases():
-    for kernel in ("auto", "brick_always", "generic", "tile_stages"):
+    for kernel in ("auto", "brick_always", "generic", "tile_stages", "axes"):
         dev.set_stage_kernel(kernel)
         for scheme in ("weno5", "weno5_fma", "eno3", "eno2", "first"):
             for counts in ((20, 35, 33), (41, 17, 18), (9, 40, 23)):

@@ -6,10 +6,13 @@ TAG=${1:-ev}
 [ -n "$SKIP_TESTS" ] || timeout 2400 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/${TAG}_gputests.log 2>&1; echo "rc $?" >> gpurun_out/${TAG}_gputests.log
 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 rm -f profiles/fp64_ops.json profiles/traffic.json
-for spec in c2:weno5:27270901 c4:weno5:214358881 c5:weno5:8242408 c2:weno5_fma:27270901; do
-  IFS=: read cfg sch nodes <<< "$spec"
+# one stage's kernels (the RK3 third stage of the 4th step): the per-axis walk
+# pipeline for WENO5 (dim kernels per stage), the brick kernel for weno5_fma
+for spec in c2:weno5:27270901:k_axis:3 c4:weno5:214358881:k_axis:4 c5:weno5:8242408:k_axis:3 \
+            c2:weno5_fma:27270901:k_stage_brick:1; do
+  IFS=: read cfg sch nodes kre nk <<< "$spec"
   SCHEME=$sch timeout 600 python scripts/variant_probe.py $cfg auto > gpurun_out/${TAG}_plain_${cfg}_$sch.log 2>&1 && \
-  SCHEME=$sch timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_brick -s 11 -c 1 \
+  SCHEME=$sch timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kre -s $((11 * nk)) -c $nk \
       -o gpurun_out/${TAG}_prof_${cfg}_$sch python scripts/variant_probe.py $cfg auto > gpurun_out/${TAG}_ncu_${cfg}_$sch.log 2>&1 && \
   python scripts/ncu_summary.py gpurun_out/${TAG}_prof_${cfg}_$sch.ncu-rep $nodes --stamp ${cfg}_$sch --traffic ${cfg}_${sch}_1 \
       > gpurun_out/${TAG}_ncu_${cfg}_$sch.json 2>&1

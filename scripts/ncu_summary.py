@@ -106,23 +106,33 @@ def main():
     rows = load(rep)
     outs = [summary(r, cells) for r in rows]
     print(json.dumps(outs if len(outs) > 1 else outs[0], indent=1))
-    last = outs[-1]
+    # a report of several launches is one stage's kernel sequence (the per-axis
+    # walk pipeline): the stamp and the traffic are the sums over them
     if stamp and cells:
         import bench   # sass_hash of the built library
 
-        frag = mangled_fragment(last["kernel"])
         path = os.path.join(ROOT, "profiles", "fp64_ops.json")
         d = json.load(open(path)) if os.path.exists(path) else {}
-        sym = bench.brick_symbol(frag)
-        d[stamp] = {"ops_per_node": last["fp64_ops_per_node"], "kernel": last["kernel"], "symbol": sym,
-                    "sass_sha256": bench.sass_hash(sym),
-                    "source": f"ncu --set full {os.path.basename(rep)}: DFMA+DMUL+DADD thread instructions / "
-                              f"{int(cells)} nodes of one launch of {last['kernel']}"}
+        ks = []
+        for o in outs:
+            sym = bench.kernel_symbol(o["kernel"])
+            ks.append({"kernel": o["kernel"], "symbol": sym, "sass_sha256": bench.sass_hash(sym),
+                       "ops_per_node": o["fp64_ops_per_node"]})
+        names = " + ".join(o["kernel"] for o in outs)
+        ent = {"ops_per_node": sum(k["ops_per_node"] for k in ks),
+               "kernel": names,
+               "source": f"ncu --set full {os.path.basename(rep)}: DFMA+DMUL+DADD thread instructions / "
+                         f"{int(cells)} nodes of one stage ({names})"}
+        if len(ks) == 1:
+            ent.update(symbol=ks[0]["symbol"], sass_sha256=ks[0]["sass_sha256"])
+        else:
+            ent["kernels"] = ks
+        d[stamp] = ent
         json.dump(d, open(path, "w"), indent=1)
     if traffic:
         path = os.path.join(ROOT, "profiles", "traffic.json")
         d = json.load(open(path)) if os.path.exists(path) else {}
-        d[traffic] = last["dram_read_bytes"] + last["dram_write_bytes"]
+        d[traffic] = sum(o["dram_read_bytes"] + o["dram_write_bytes"] for o in outs)
         json.dump(d, open(path, "w"), indent=1)
 
 

@@ -29,12 +29,14 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
-@pytest.fixture(params=["auto", "brick_always", "generic", "tile_stages"])
+@pytest.fixture(params=["auto", "brick_always", "generic", "tile_stages", "axes"])
 def stage_kernel(request):
     """Run a GPU parity test under every fused-stage kernel family: the
     default dispatch (small grids: the tile kernel, an integration interval
-    in one persistent launch), the brick kernels forced even on tiny grids,
-    the per-node generic kernel, and the tile kernel launched per stage."""
+    in one persistent launch; large WENO5 grids: the per-axis walk
+    pipeline), the brick kernels forced even on tiny grids, the per-node
+    generic kernel, the tile kernel launched per stage, and the per-axis
+    walk pipeline forced on every size."""
     from paper_2411_03501_b200 import device as dev
 
     old = dev.set_stage_kernel(request.param)

@@ -236,5 +236,9 @@ def test_bench_config_table():
     assert bench.CONFIGS == ("c1", "c2", "c3", "c4", "c5")
     assert bench.parse([]).config == "c2"
     assert abs(bench.BYTES_RK3 - 64 / 3) < 1e-12 and bench.BYTES_RK2 == 20.0
-    assert bench.brick_symbol("k_stage_brickILi3ELi3ELi2ELi0ELi2EE") == \
+    assert bench.kernel_symbol("void k_stage_brick<3, 3, 2, 0, 2>(StageArgs, int)") == \
         "_ZN2hj13k_stage_brickILi3ELi3ELi2ELi0ELi2EEEvNS_9StageArgsEi"
+    assert bench.kernel_symbol("void hj::k_axis_col<3, 4, 4, 0>(hj::StageArgs, hj::AxesScratch)") == \
+        "_ZN2hj10k_axis_colILi3ELi4ELi4ELi0EEEvNS_9StageArgsENS_11AxesScratchE"
+    assert bench.kernel_symbol("void k_axis_x<3>(StageArgs, AxesScratch)") == \
+        "_ZN2hj8k_axis_xILi3EEEvNS_9StageArgsENS_11AxesScratchE"
