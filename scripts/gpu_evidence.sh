@@ -34,3 +34,4 @@ timeout 300 python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${TAG}_launches_c2.csv \
     python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-tolerance-mode > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo finished
+HJ_LIB=check timeout 900 python scripts/bounds_check.py > gpurun_out/${TAG}_bounds.txt 2>&1; echo "rc $?" >> gpurun_out/${TAG}_bounds.txt
