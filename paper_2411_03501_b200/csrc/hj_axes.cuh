@@ -119,19 +119,22 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, con
 template <int DIM>
 struct AxisColSmem {
   static constexpr int NS = DIM + 3;   // ring streams: P[0..DIM-3], PX, D, DX, y0, mask
-  static constexpr size_t bytes(int mode) {
+  // shared memory of a column kernel with SEGC-node segments: the staged
+  // column rows, then the two-node ring (mode 1: D; mode 2: NS streams)
+  static constexpr size_t bytes(int mode, int segc) {
     return sizeof(double) * (size_t)AX_THREADS *
-           (AX_ROWS + (mode == 1 ? AX_SEG : 0) + (mode == 2 ? 2 * NS : 0));
+           ((segc + 6) + (mode == 1 ? 2 : 0) + (mode == 2 ? 2 * NS : 0));
   }
 };
 
-template <int SCHEME, int HAM, int DIM, int AXIS>
+template <int SCHEME, int HAM, int DIM, int AXIS, int SEGC>
 __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, const AxesScratch S) {
   constexpr int axis = AXIS;
   constexpr int MODE = (AXIS == DIM - 2) ? 2 : (AXIS == 0 ? 0 : 1);
   constexpr int NS = AxisColSmem<DIM>::NS;
-  extern __shared__ __align__(16) double cs[];   // [AX_ROWS][256] column, then D (mode 1) / the ring (mode 2)
-  double* const extra = cs + AX_ROWS * AX_THREADS;
+  constexpr int ROWS = SEGC + 6;
+  extern __shared__ __align__(16) double cs[];   // [ROWS][256] column, then the ring (modes 1, 2)
+  double* const extra = cs + ROWS * AX_THREADS;
   const GridArgs& G = P.g;
   const long long inner = G.stride[axis];
   const int na = G.n[axis];
@@ -143,8 +146,8 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
   const long long colbase = o * (na * inner) + i;   // field offset of node 0 of this column
   const double* col = P.y_in + colbase;
   const AxisView A = G.ax[axis];
-  const int z0 = blockIdx.y * AX_SEG;
-  const int zmax = min(AX_SEG, na - z0);
+  const int z0 = blockIdx.y * SEGC;
+  const int zmax = min(SEGC, na - z0);
   const bool innerseg = z0 >= 3 && z0 + zmax + 3 <= na;   // CTA-uniform
   const int t = threadIdx.x;
   if (on) {
@@ -156,30 +159,46 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
     } else {
       stage_line(col, A, z0, zmax, cs + t, AX_THREADS);
     }
-    if constexpr (MODE == 1) {
-      for (int j = 0; j < zmax; ++j) {
-        const long long off = colbase + (long long)(z0 + j) * inner;
-        HJ_CHK(P, aux, S.d + off, 8);
-        cp_async8(&extra[j * AX_THREADS + t], S.d + off);
-      }
-    }
   }
   cp_async_wait_all();
   if (on && !innerseg) ghost_fill(A, z0, zmax, cs + t, AX_THREADS);   // own column: no barrier needed
   __syncthreads();
   const double ah = P.alpha_half[axis];
   auto ld = [&](int k) -> double { return cs[(k + 3) * AX_THREADS + t]; };
-  if constexpr (MODE < 2) {
+  if constexpr (MODE == 0) {
     auto emit = [&](int j, double L, double R) {
       if (j < zmax) {
         const long long off = colbase + (long long)(z0 + j) * inner;
         HJ_CHK(P, aux, S.d + off, 8);
         HJ_CHK(P, aux, S.p[axis] + off, 8);
         S.p[axis][off] = 0.5 * (L + R);                                               // term.py:101
-        S.d[off] = (MODE == 0 ? 0.0 : extra[j * AX_THREADS + t]) + ah * (R - L);      // term.py:84-86
+        S.d[off] = 0.0 + ah * (R - L);                                                // term.py:84-86
       }
     };
-    if (on) line_walk<SCHEME, 1, AX_SEG>(ld, G.sp[axis], emit, zmax);
+    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
+  } else if constexpr (MODE == 1) {
+    // the running sum's D of node j through a two-node cp.async ring
+    auto issue = [&](int j) {
+      if (on && j < zmax) {
+        const long long off = colbase + (long long)(z0 + j) * inner;
+        HJ_CHK(P, aux, S.d + off, 8);
+        cp_async8(extra + (j & 1) * AX_THREADS + t, S.d + off);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    issue(1);
+    auto emit = [&](int j, double L, double R) {
+      if (j >= zmax) return;
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      const long long off = colbase + (long long)(z0 + j) * inner;
+      HJ_CHK(P, aux, S.p[axis] + off, 8);
+      S.p[axis][off] = 0.5 * (L + R);                                                 // term.py:101
+      S.d[off] = extra[(j & 1) * AX_THREADS + t] + ah * (R - L);                      // term.py:84-86
+      issue(j + 2);   // (the slot's value is consumed by the store above)
+    };
+    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     // node indices of this column (axis `axis` varies along the walk)
     int ix[HJ_MAX_DIM] = {0, 0, 0, 0, 0};
@@ -268,7 +287,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
         if (!finite(out)) flags |= HJ_NF_OUTPUT;
       }
     };
-    if (on) line_walk<SCHEME, 1, AX_SEG>(ld, G.sp[axis], emit, zmax);
+    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (P.stats) {   // every thread of the CTA (warp-synchronous reduction)
       long long dmy[DIM];
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
 
 // The pipeline of one stage.  Covers whole-grid launches (every axis-0 plane,
 // no exchanged halos) of dims 3 and 4; *handled = false otherwise.
-template <int SCHEME, int HAM, int DIM>
+template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG>
 static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch) {
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
@@ -291,11 +310,22 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   S.d = scratch + 2 * span;
   for (int a = 0; a < DIM - 2; ++a) S.p[a] = scratch + (3 + a) * span;
   const size_t xsmem = (size_t)(AX_ROWS + 2 * AX_SEG) * AX_PITCH * sizeof(double);
+  using CS = AxisColSmem<DIM>;
   static std::atomic<bool> configured[64];
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaError_t e = cudaSuccess;
   if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(k_axis_x<SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
+    e = cudaFuncSetAttribute(k_axis_x<SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 0, SEGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)CS::bytes(0, SEGC));
+    if (e == cudaSuccess && DIM == 4)
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 1, SEGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)CS::bytes(1, SEGC));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::bytes(2, SEGC));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev].store(true, std::memory_order_release);
   }
@@ -306,29 +336,15 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   const long long rows = (long long)G.batch * (G.cells / G.n[X]);
   k_axis_x<SCHEME><<<dim3((unsigned)((rows + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[X] + AX_SEG - 1) / AX_SEG)),
                      AX_THREADS, xsmem, s>>>(Q, S);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   auto grid_of = [&](int a) {
     const long long ncol = (long long)G.batch * G.cells / G.n[a];
-    return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + AX_SEG - 1) / AX_SEG));
+    return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + SEGC - 1) / SEGC));
   };
-  using CS = AxisColSmem<DIM>;
-  static std::atomic<bool> col_configured[64];
-  if (dev < 0 || dev >= 64 || !col_configured[dev].load(std::memory_order_acquire)) {
-    e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)CS::bytes(0));
-    if (e == cudaSuccess && DIM == 4)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)CS::bytes(1));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)CS::bytes(2));
-    if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) col_configured[dev].store(true, std::memory_order_release);
-  }
-  k_axis_col<SCHEME, HAM, DIM, 0><<<grid_of(0), AX_THREADS, CS::bytes(DIM == 3 ? 0 : 0), s>>>(Q, S);
-  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1><<<grid_of(1), AX_THREADS, CS::bytes(1), s>>>(Q, S);
-  k_axis_col<SCHEME, HAM, DIM, DIM - 2><<<grid_of(DIM - 2), AX_THREADS, CS::bytes(2), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, 0, SEGC><<<grid_of(0), AX_THREADS, CS::bytes(0, SEGC), s>>>(Q, S);
+  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1, SEGC><<<grid_of(1), AX_THREADS, CS::bytes(1, SEGC), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC><<<grid_of(DIM - 2), AX_THREADS, CS::bytes(2, SEGC), s>>>(Q, S);
   return cudaGetLastError();
 }
 
