@@ -59,7 +59,8 @@ static int fail(int code, const char* fmt, ...) {
 }
 
 namespace hj {
-bool axes_applies(int scheme, const StageArgs& P);   // hj_fast.cu
+bool axes_applies(int scheme, const StageArgs& P, bool allow_halo);   // hj_fast.cu
+cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int parts);   // hj_axes_weno.cu
 // for the other translation units of the library (hj_dd.cu): set the
 // thread-local message / count launches made outside this file
 int set_error(int code, const char* msg) {
@@ -312,6 +313,9 @@ int hj_weno5_workspace(const hj_grid* g, int axis, int side, int eps_mode, const
 // a row r covers planes [r*unit, r*unit+unit) and reads `reach` planes
 // further on each side.
 constexpr int STAGE_PLANES = 3;   // internal: an explicit plane range (hj_stage_planes)
+// internal: the two halves of a per-axis-pipeline slab stage (hj_dd_stage):
+// the contiguous-axis kernel (reads no exchanged plane), then the column kernels
+constexpr int STAGE_AXES_X = 4, STAGE_AXES_REST = 5;
 
 static RowSet row_set(int n0, int unit, int reach, int halo_lo, int halo_hi, int part) {
   const int nrows = (n0 + unit - 1) / unit;
@@ -361,7 +365,8 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
                   (long long)plo, (long long)phi, (long long)n0);
     if (plo == phi) return HJ_OK;
   }
-  set_rows(P, w, part, plo, phi);
+  const bool axes_split = part == STAGE_AXES_X || part == STAGE_AXES_REST;
+  set_rows(P, w, axes_split ? HJ_PART_ALL : part, plo, phi);
   rc = check_ham(ham, P.g.dim);
   if (rc) return rc;
   if (!alpha) return fail(HJ_EINVAL, "alpha is NULL");
@@ -395,7 +400,18 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
   }
   cudaStream_t s = (cudaStream_t)stream;
   const size_t span = (size_t)(P.g.batch_stride * (P.g.batch - 1) + P.g.cells);
-  const bool axes = axes_applies(scheme, P);
+  if (axes_split) {
+    // one half of a slab stage on the per-axis walk pipeline (same stream, so
+    // the same scratch for both halves)
+    if (!axes_applies(scheme, P, true)) return fail(HJ_EINVAL, "stage does not run the per-axis walk pipeline");
+    P.aux0 = scratch_for(s, (size_t)(P.g.dim + 1) * span);
+    if (!P.aux0) return fail(HJ_ECUDA, "no scratch for the per-axis walk pipeline");
+    set_extents(P, g);
+    bool handled = false;
+    cudaError_t e = launch_axes_weno5(P, s, &handled, part == STAGE_AXES_X ? 1 : 2);
+    return cuda_status(e, "hj_stage (per-axis pipeline)", part == STAGE_AXES_X ? 1 : (uint64_t)(P.g.dim - 1));
+  }
+  const bool axes = axes_applies(scheme, P, false);
   if (axes) {
     // per-axis walk pipeline (hj_axes.cuh): dim + 1 field-sized scratch arrays
     P.aux0 = scratch_for(s, (size_t)(P.g.dim + 1) * span);
@@ -617,6 +633,25 @@ int hj_divided_differences(const hj_grid* g, int axis, int width, int order, con
 }  // extern "C"
 
 namespace hj {
+// a slab stage on the per-axis walk pipeline, around its halo exchange
+// (hj_dd_stage): axes_slab_applies says whether it runs there, then
+// stage_axes_part(.., 1) launches the contiguous-axis kernel and
+// stage_axes_part(.., 2) the column kernels
+bool axes_slab_applies(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, int stage,
+                       const double* y_in, const double* y0, double* y_out) {
+  StageArgs P;
+  if (stage_impl(g, scheme, ham, alpha, 0.0, stage, y_in, y0, y_out, nullptr, HJ_MASK_NONE, nullptr, 0,
+                 HJ_PART_ALL, 0, 0, nullptr, &P))
+    return false;
+  return axes_applies(scheme, P, true);
+}
+int stage_axes_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                    const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                    hj_stats* stats, int32_t tag, int which, void* stream) {
+  return stage_impl(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag,
+                    which == 1 ? STAGE_AXES_X : STAGE_AXES_REST, 0, 0, stream);
+}
+
 // hj_stage's validation and argument build without the launch
 int stage_args(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
                const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,

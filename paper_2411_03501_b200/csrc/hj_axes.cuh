@@ -300,8 +300,10 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
 
 // The pipeline of one stage.  Covers whole-grid launches (every axis-0 plane,
 // no exchanged halos) of dims 3 and 4; *handled = false otherwise.
+// parts: bit 0 the contiguous-axis kernel, bit 1 the column kernels (a slab
+// stage launches them on either side of its halo exchange, hj_dd_stage)
 template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG>
-static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch) {
+static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch, int parts = 3) {
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
   AxesScratch S{};
@@ -334,10 +336,14 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   Q.bc.aux = Extent{scratch, scratch + (DIM + 1) * span};
   const int X = DIM - 1;
   const long long rows = (long long)G.batch * (G.cells / G.n[X]);
-  k_axis_x<SCHEME><<<dim3((unsigned)((rows + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[X] + AX_SEG - 1) / AX_SEG)),
-                     AX_THREADS, xsmem, s>>>(Q, S);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (parts & 1) {
+    k_axis_x<SCHEME><<<dim3((unsigned)((rows + AX_THREADS - 1) / AX_THREADS),
+                            (unsigned)((G.n[X] + AX_SEG - 1) / AX_SEG)),
+                       AX_THREADS, xsmem, s>>>(Q, S);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (!(parts & 2)) return cudaSuccess;
   auto grid_of = [&](int a) {
     const long long ncol = (long long)G.batch * G.cells / G.n[a];
     return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + SEGC - 1) / SEGC));

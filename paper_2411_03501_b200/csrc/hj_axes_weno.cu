@@ -3,23 +3,24 @@
 
 namespace hj {
 template <int SEGC>
-static cudaError_t axes_weno5(const StageArgs& P, cudaStream_t s) {
+static cudaError_t axes_weno5(const StageArgs& P, cudaStream_t s, int parts) {
   double* scratch = P.aux0;
   if (P.g.dim == 4) {
-    if (P.ham.kind == HJ_HAM_DI4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC>(P, s, scratch);
-    return launch_axes_t<HJ_WENO5, HJ_HAM_ADVECTION, 4, SEGC>(P, s, scratch);
+    if (P.ham.kind == HJ_HAM_DI4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC>(P, s, scratch, parts);
+    return launch_axes_t<HJ_WENO5, HJ_HAM_ADVECTION, 4, SEGC>(P, s, scratch, parts);
   }
   switch (P.ham.kind) {
-    case HJ_HAM_AIR3D: return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC>(P, s, scratch);
-    case HJ_HAM_ROCKETS: return launch_axes_t<HJ_WENO5, HJ_HAM_ROCKETS, 3, SEGC>(P, s, scratch);
-    case HJ_HAM_ROCKETS_EXTREMAL: return launch_axes_t<HJ_WENO5, HJ_HAM_ROCKETS_EXTREMAL, 3, SEGC>(P, s, scratch);
-    default: return launch_axes_t<HJ_WENO5, HJ_HAM_ADVECTION, 3, SEGC>(P, s, scratch);
+    case HJ_HAM_AIR3D: return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC>(P, s, scratch, parts);
+    case HJ_HAM_ROCKETS: return launch_axes_t<HJ_WENO5, HJ_HAM_ROCKETS, 3, SEGC>(P, s, scratch, parts);
+    case HJ_HAM_ROCKETS_EXTREMAL:
+      return launch_axes_t<HJ_WENO5, HJ_HAM_ROCKETS_EXTREMAL, 3, SEGC>(P, s, scratch, parts);
+    default: return launch_axes_t<HJ_WENO5, HJ_HAM_ADVECTION, 3, SEGC>(P, s, scratch, parts);
   }
 }
 
 // (32-node column segments measured +1.5 % C4, -1.8 % C5, -0.2 % C2: 16 kept)
-cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled) {
+cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int parts) {
   *handled = true;
-  return axes_weno5<AX_SEG>(P, s);
+  return axes_weno5<AX_SEG>(P, s, parts);
 }
 }  // namespace hj

@@ -33,6 +33,11 @@
 namespace hj {
 int set_error(int code, const char* msg);
 void count_launches(uint64_t n);
+bool axes_slab_applies(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, int stage,
+                       const double* y_in, const double* y0, double* y_out);
+int stage_axes_part(const hj_grid* g, int scheme, const hj_ham* ham, const double* alpha, double dt, int stage,
+                    const double* y_in, const double* y0, double* y_out, const double* mask_prev, int mask,
+                    hj_stats* stats, int32_t tag, int which, void* stream);
 }  // namespace hj
 
 using namespace hj;
@@ -253,6 +258,17 @@ int hj_dd_stage(hj_dd* dd, const hj_grid* g, int scheme, const hj_ham* ham, cons
   cudaStream_t s = (cudaStream_t)stream;
   if (!g->halo_lo && !g->halo_hi)
     return hj_stage(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, stream);
+  // per-axis walk pipeline (large WENO5 slabs): only the axis-0 walk reads
+  // exchanged planes, so the contiguous-axis kernel overlaps the exchange and
+  // the column kernels follow it -- no CORE/RIM split
+  if (overlap && axes_slab_applies(g, scheme, ham, alpha, stage, y_in, y0, y_out)) {
+    int rc = post_exchange(dd, g, y_in, s);
+    if (rc) return rc;
+    rc = stage_axes_part(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, 1, stream);
+    if (rc) return rc;
+    HJ_CUDA(cudaStreamWaitEvent(s, dd->ev_halo, 0), "hj_dd_stage: cudaStreamWaitEvent");
+    return stage_axes_part(g, scheme, ham, alpha, dt, stage, y_in, y0, y_out, mask_prev, mask, stats, tag, 2, stream);
+  }
   int rc = post_exchange(dd, g, y_in, s);
   if (rc) return rc;
   if (overlap) {

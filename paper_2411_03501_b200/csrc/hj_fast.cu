@@ -8,7 +8,7 @@ cudaError_t launch_brick_weno5(const StageArgs& P, cudaStream_t s, bool* handled
 cudaError_t launch_brick_eno(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
 cudaError_t launch_brick_weno5_fma(const StageArgs& P, cudaStream_t s, bool* handled, int variant);
 cudaError_t launch_tile(int scheme, const StageArgs& P, cudaStream_t s, bool* handled);
-cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled);
+cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int parts);
 
 // HJ_STAGE_KERNEL selects the stage kernel for A/B measurements:
 //   unset / "brick" : brick-tiled kernels, 2 CTAs per SM (default)
@@ -50,11 +50,14 @@ int set_stage_variant(int v) {
 // statistics) -- by default those of brick size (measured faster than the
 // brick kernels at 301^3, 121^4 and 8 x 101^3: DESIGN.md); "axes" forces it
 // on every size (tests).  It needs (dim + 1) field-sized scratch arrays.
-bool axes_applies(int scheme, const StageArgs& P) {
+// allow_halo: a multi-GPU slab stage split around its halo exchange
+// (hj_dd_stage: the contiguous-axis kernel overlaps the exchange; only the
+// axis-0 walk reads exchanged planes).
+bool axes_applies(int scheme, const StageArgs& P, bool allow_halo) {
   const int v = stage_variant();
   if ((v != 1 && v != 9) || scheme != HJ_WENO5) return false;
   if ((P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return false;
-  if (P.g.ax[0].halo_lo || P.g.ax[0].halo_hi) return false;
+  if (!allow_halo && (P.g.ax[0].halo_lo || P.g.ax[0].halo_hi)) return false;
   if (P.zp.lo != 0 || P.zp.cnt != P.g.n[0]) return false;
   if (P.g.batch > 1 && P.g.batch_stride != P.g.cells) return false;
   bool ham_ok = false;
@@ -77,7 +80,7 @@ bool axes_applies(int scheme, const StageArgs& P) {
 cudaError_t launch_stage_fast(int scheme, const StageArgs& P, cudaStream_t s, bool* handled) {
   *handled = false;
   const int variant = stage_variant();
-  if (P.aux0 && axes_applies(scheme, P)) return launch_axes_weno5(P, s, handled);
+  if (P.aux0 && axes_applies(scheme, P, false)) return launch_axes_weno5(P, s, handled, 3);
   if (variant == 0 || (P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return cudaSuccess;
   // too few bricks to occupy the SMs (small grids such as C1's 51x51x36):
   // the per-node kernel exposes more parallelism

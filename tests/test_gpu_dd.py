@@ -118,3 +118,32 @@ def test_abi_rejects_thin_halo_and_missing_neighbour():
         assert rc == _lib.HJ_EINVAL and b"neighbour" in lib.hj_last_error()
     finally:
         lib.hj_dd_free(h)
+
+
+@pytest.mark.parametrize("dim", [3, 4])
+def test_self_ring_per_axis_pipeline(dim):
+    """The slab stage on the per-axis walk pipeline (hj_dd_stage: the
+    contiguous-axis kernel overlaps the exchange, the column kernels follow
+    it), forced on a small grid, against the single domain under the same
+    kernel family and under the default dispatch."""
+    if dim == 3:
+        g, y0 = _periodic3()
+        cfg = hj.advection_term_config([1.0, -0.5, 0.25], scheme="weno5")
+    else:
+        g = hj.create_grid((0.0, -1.0, -1.0, -1.0), (2 * np.pi, 1.0, 1.0, 1.0), (24, 12, 17, 18),
+                           periodic_axes={0})
+        cfg = hj.advection_term_config([0.5, -0.25, 0.75, 1.0], scheme="weno5")
+        x = g.axis_nodes[0][:, None, None, None]
+        y0 = np.broadcast_to(np.cos(x) + 0.2 * g.axis_nodes[3][None, None, None, :], g.counts).copy()
+    dt = 0.5 / float(np.sum(cfg.partials.alphas(0.0, g) / g.spacings))
+    old = dev.set_stage_kernel("axes")
+    try:
+        ref = dev.to_host(_steps(FusedIntegrator(g, cfg), dev.to_dev(y0), dt, 2))
+        run = SlabIntegrator(g, cfg, 0, 1, transport="nccl", overlap=True, self_ring=True)
+        got = dev.to_host(run.owned(_steps(run, run.scatter(y0), dt, 2)))
+        run.transport.close()
+    finally:
+        dev.set_stage_kernel(old)
+    default = dev.to_host(_steps(FusedIntegrator(g, cfg), dev.to_dev(y0), dt, 2))
+    assert np.array_equal(ref, got)
+    assert np.array_equal(default, got)
