@@ -169,7 +169,7 @@ static int check_ham(const hj_ham* ham, int dim) {
 // SCRATCH_ENTRIES buffers live at once: the least recently used one is freed
 // (cudaFree synchronises the device, so a buffer is never released while a
 // kernel still uses it).
-constexpr size_t SCRATCH_ENTRIES = 4;
+constexpr size_t SCRATCH_ENTRIES = 16;   // (a batch solve runs one stream per problem)
 static double* scratch_for(cudaStream_t s, size_t n_doubles) {
   struct Entry {
     int dev;

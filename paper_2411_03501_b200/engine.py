@@ -395,6 +395,13 @@ class FusedIntegrator:
     def _read_stats(self):
         return self.stats.read()
 
+    def raise_pending(self, order: int, t0: float, t1: float, y: torch.Tensor, opts) -> None:
+        """The error check integrate(check=True) does after a native run, for a
+        caller that ran it with check=False on a stream of its own and has
+        synchronised since (the device flags are still those of that run)."""
+        bound = step_bound(self._alphas_at(t0, y, 0), self.g)
+        self._raise_pending(self._replay_times(order, t0, t1, bound, opts), warn=bound == np.inf)
+
     def _raise_pending(self, times: dict[int, float], warn: bool = False) -> None:
         """Turn the device flags into the exception the reference raises first."""
         s = self._read_stats()

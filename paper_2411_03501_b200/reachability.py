@@ -355,6 +355,74 @@ def _batch_runner(g: Grid, cfg: TermConfig, batch: int):
     return hit[1], hit[2], hit[3]
 
 
+def _stream_runner(g: Grid, cfg: TermConfig, batch: int):
+    """(one FusedIntegrator per problem, one stream per problem, per-problem
+    device inputs) of (grid, cfg, batch, device), reused across calls."""
+    from .engine import FusedIntegrator
+
+    fi, staging, pool = _batch_runner(g, cfg, batch)   # (the pinned staging and copy pool)
+    key = ("streams", id(cfg), batch, torch.cuda.current_device())
+    per = _BATCH.setdefault(g, {})
+    hit = per.get(key)
+    if hit is None or hit[0] is not cfg:
+        fis = [FusedIntegrator(g, cfg) for _ in range(batch)]
+        streams = [torch.cuda.Stream() for _ in range(batch)]
+        ins = [torch.empty(tuple(g.counts), dtype=dev.F64, device=dev.device()) for _ in range(batch)]
+        hit = (cfg, fis, streams, ins)
+        per[key] = hit
+    return hit[1], hit[2], hit[3], staging, pool
+
+
+def _solve_batch_streamed(g: Grid, arrs, cfg: TermConfig, horizon: float, order: int, opts, use_min: bool):
+    """One interval of every problem of the batch, final states only: problem b
+    runs on its own stream -- host copy into pinned staging, H2D, the native
+    integration (mask fused in the last stage), D2H -- so the copies of one
+    problem overlap the stages of the others (the lockstep batch waits for
+    the whole batch's input before its first stage and for its last stage
+    before any output).  Errors are read from each problem's device flags
+    after all streams finish: the reference's non-finite-input ValueError,
+    or the interval's RuntimeError."""
+    B = len(arrs)
+    fis, streams, ins, staging, pool = _stream_runner(g, cfg, B)
+    st = staging.numpy()
+    # host copies into pinned staging problem by problem, each split across the
+    # pool's threads, so problem 0's DMA can start after 1/B of the copying
+    n0 = st.shape[1]
+    parts = min(8, n0)
+    bounds = [n0 * k // parts for k in range(parts + 1)]
+    futs = [[pool.submit(np.copyto, st[b, bounds[k]:bounds[k + 1]], a[bounds[k]:bounds[k + 1]])
+             for k in range(parts)] for b, a in enumerate(arrs)]
+    out = torch.empty((B,) + tuple(g.counts), dtype=dev.F64, pin_memory=True)
+    main = torch.cuda.current_stream()
+    for b in range(B):
+        s = streams[b]
+        s.wait_stream(main)
+        for f in futs[b]:
+            f.result()
+        with torch.cuda.stream(s):
+            ins[b].copy_(staging[b], non_blocking=True)
+            try:
+                res = fis[b].integrate(order, (0.0, horizon), ins[b], opts, mask_prev=ins[b], use_min=use_min,
+                                       check=False)
+            except Exception as err:
+                raise RuntimeError(f"tube interval 1 failed: {err}") from err
+            out[b].copy_(res.y, non_blocking=True)
+            res.y.record_stream(s)
+    for s in streams:
+        main.wait_stream(s)
+    main.synchronize()
+    for b in range(B):
+        try:
+            fis[b].raise_pending(order, 0.0, horizon, ins[b], opts)
+        except ValueError as err:
+            if str(err) == "field contains non-finite values":
+                raise
+            raise RuntimeError(f"tube interval 1 failed: {err}") from err
+        except Exception as err:
+            raise RuntimeError(f"tube interval 1 failed: {err}") from err
+    return out.numpy()
+
+
 def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_steps: int, order: int = 3,
                      opts: IntegratorOptions | None = None, keep_snapshots: bool = True):
     """A batch of independent tubes sharing grid and dynamics (BASELINE C5:
@@ -370,6 +438,10 @@ def solve_tube_batch(g: Grid, targets, cfg: TermConfig, horizon: float, global_s
         if a.shape != tuple(g.counts):
             raise ValueError(f"targets have shape {a.shape}, grid needs {g.counts}")
     opts = opts or IntegratorOptions()
+    if not keep_snapshots and global_steps == 1 and len(arrs) > 1 and horizon > 0.0:
+        # final states of one interval: per-problem streams overlap the copies with the stages
+        return _solve_batch_streamed(g, arrs, cfg, float(horizon), order, opts,
+                                     cfg.approximation_sign == "over"), (0.0, horizon)
     fi, staging, pool = _batch_runner(g, cfg, len(arrs))
     # the targets go to pinned staging on host threads (NumPy copies release
     # the GIL), then one DMA; finiteness is checked on the device
