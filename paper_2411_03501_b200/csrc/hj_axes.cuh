@@ -210,6 +210,11 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
         rem -= (long long)ix[a] * G.stride[a];
       }
     }
+    double cin[4] = {0.0, 0.0, 0.0, 0.0};
+    if (on) {
+      ix[axis] = z0;
+      ham_inputs<HAM, DIM>(P.ham, G.nodes, ix, cin);
+    }
     const double* __restrict__ mp = P.mask_prev;
     const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
     const bool need_m = P.mask != HJ_MASK_NONE;
@@ -248,7 +253,11 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
       asm volatile("cp.async.wait_group 1;" ::: "memory");   // node j's copies have landed
       const double* slot = extra + (j & 1) * NS * AX_THREADS + t;
       const long long off = colbase + (long long)(z0 + j) * inner;
-      ix[axis] = z0 + j;
+      // H's node-table inputs: the column's constant ones were read once
+      // (cin below); only the walk axis' coordinate changes per node
+      if constexpr (HAM == HJ_HAM_AIR3D && axis == 1) cin[1] = G.nodes[1][z0 + j];
+      if constexpr ((HAM == HJ_HAM_ROCKETS || HAM == HJ_HAM_ROCKETS_EXTREMAL) && axis == 0) cin[0] = G.nodes[0][z0 + j];
+      if constexpr (HAM == HJ_HAM_DI4 && axis == 2) cin[0] = G.nodes[2][z0 + j];
       double pv[DIM];
 #pragma unroll
       for (int a = 0; a < DIM - 2; ++a) pv[a] = slot[a * AX_THREADS];
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
       pv[DIM - 1] = slot[(DIM - 2) * AX_THREADS];
       // term.py:84-86 order: (((0 + d0) + ...) + d_{dim-2}) + d_{dim-1}
       const double dsum = (slot[(DIM - 1) * AX_THREADS] + ah * (R - L)) + slot[DIM * AX_THREADS];
-      const double H = hamiltonian<HAM, DIM>(P.ham, G.nodes, ix, pv);
+      const double H = ham_eval<HAM, DIM>(P.ham, cin, pv);
       if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
       const double delta = dsum - H;                                         // term.py:113
       const double yv = ld(j);
