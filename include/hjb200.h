@@ -277,11 +277,15 @@ int hj_tube_check(int64_t count, const double* prev, const double* v, const doub
  * n random/special operand pairs, *d_mismatch += #{div_by(a,b) != a/b} (bitwise). */
 int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, void* stream);
 /* Stage-kernel family (A/B measurements and test coverage): 0 per-node generic
- * kernel, 1 brick kernels when the grid has enough bricks (default), 2 brick
- * WENO5 kernel at 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid, 4 WENO5
- * walks rolled, 5 timing bound only (WENO5 bricks after a CTA's first skip
- * their global->shared loads: WRONG results), 6 brick kernels without the L2
- * prefetch of the next brick; -1 reads HJ_STAGE_KERNEL from the environment.
+ * kernel, 1 default dispatch (grids of brick size: the per-axis walk pipeline
+ * for WENO5, the brick kernels otherwise; small 3-D grids: the tile kernel,
+ * an hj_integrate interval as one persistent launch), 2 brick WENO5 kernel at
+ * 1 CTA/SM, 3 brick kernels for every 3-D/4-D grid, 4 WENO5 walks rolled,
+ * 5 timing bound only (WENO5 bricks after a CTA's first skip their
+ * global->shared loads: WRONG results), 6 brick kernels without the L2
+ * prefetch of the next brick, 7 the brick A/B slot, 8 small 3-D grids: tile
+ * kernel per stage (no persistent launch), 9 the per-axis walk pipeline for
+ * every WENO5 grid size; -1 reads HJ_STAGE_KERNEL from the environment.
  * Returns the previous setting. */
 int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
