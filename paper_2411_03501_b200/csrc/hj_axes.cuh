@@ -43,7 +43,9 @@ struct AxesScratch {
 // transposed (warp w loads rows 32w .. 32w+31, lanes along the row: 22
 // consecutive doubles per load), thread t walks row t from shared memory, the
 // (p, d) results are staged and written back row-wise (coalesced).
-template <int SCHEME>
+// WU: walk steps per loop iteration (2: the window state rolls through
+// renamed registers instead of moves; hj_weno_line.cuh)
+template <int SCHEME, int WU = 1>
 __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, const AxesScratch S) {
   extern __shared__ __align__(16) double axs[];
   double* stg = axs;                                  // [AX_ROWS][AX_PITCH]
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, con
         sd[i * AX_PITCH + t] = ah * (R - L);    // term.py:85-86 (added last: axis X is the last axis)
       }
     };
-    line_walk<SCHEME, 1, AX_SEG>(ld, G.sp[X], emit, zmax);
+    line_walk<SCHEME, WU, AX_SEG>(ld, G.sp[X], emit, zmax);
   }
   __syncthreads();
   // write back row-wise: half-warps per row, lanes along the segment
@@ -127,8 +129,8 @@ struct AxisColSmem {
   }
 };
 
-template <int SCHEME, int HAM, int DIM, int AXIS, int SEGC>
-__global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, const AxesScratch S) {
+template <int SCHEME, int HAM, int DIM, int AXIS, int SEGC, int WU = 1, int MINB = 2>
+__global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P, const AxesScratch S) {
   constexpr int axis = AXIS;
   constexpr int MODE = (AXIS == DIM - 2) ? 2 : (AXIS == 0 ? 0 : 1);
   constexpr int NS = AxisColSmem<DIM>::NS;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
         S.d[off] = 0.0 + ah * (R - L);                                                // term.py:84-86
       }
     };
-    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
+    if (on) line_walk<SCHEME, WU, SEGC>(ld, G.sp[axis], emit, zmax);
   } else if constexpr (MODE == 1) {
     // the running sum's D of node j through a two-node cp.async ring
     auto issue = [&](int j) {
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
       S.d[off] = extra[(j & 1) * AX_THREADS + t] + ah * (R - L);                      // term.py:84-86
       issue(j + 2);   // (the slot's value is consumed by the store above)
     };
-    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
+    if (on) line_walk<SCHEME, WU, SEGC>(ld, G.sp[axis], emit, zmax);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     // node indices of this column (axis `axis` varies along the walk)
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
         if (!finite(out)) flags |= HJ_NF_OUTPUT;
       }
     };
-    if (on) line_walk<SCHEME, 1, SEGC>(ld, G.sp[axis], emit, zmax);
+    if (on) line_walk<SCHEME, WU, SEGC>(ld, G.sp[axis], emit, zmax);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (P.stats) {   // every thread of the CTA (warp-synchronous reduction)
       long long dmy[DIM];
@@ -311,8 +313,16 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_col(const StageArgs P, c
 // no exchanged halos) of dims 3 and 4; *handled = false otherwise.
 // parts: bit 0 the contiguous-axis kernel, bit 1 the column kernels (a slab
 // stage launches them on either side of its halo exchange, hj_dd_stage)
-template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG>
+// WU: walk two steps per loop iteration in the contiguous-axis kernel (bit 0),
+// the last-axis kernel (bit 1), the axis-0 / middle-axis column kernels (bit
+// 2); bit 3: column kernels compiled for 3 CTAs per SM.  Default: bit 2 only
+// (A/B on one B200, profiles/r02_raw/kernel_variant_ab.txt: C2 +1.9 %, C4
+// +1.9 %, C5 +-0; the unrolled contiguous-axis walk: C2 +2.0 %, C4 -4.7 %,
+// C5 -0.6 %; the unrolled last-axis walk -0.4 .. -1.2 %; 3 CTAs per SM spill
+// at 80 registers: -32 .. -40 %)
+template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG, int WU = 4>
 static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch, int parts = 3) {
+  constexpr int XU = (WU & 1) ? 2 : 1, LU = (WU & 2) ? 2 : 1, CU = (WU & 4) ? 2 : 1, MB = (WU & 8) ? 3 : 2;
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
   AxesScratch S{};
@@ -327,15 +337,15 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   cudaGetDevice(&dev);
   cudaError_t e = cudaSuccess;
   if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
-    e = cudaFuncSetAttribute(k_axis_x<SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
+    e = cudaFuncSetAttribute(k_axis_x<SCHEME, XU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 0, SEGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 0, SEGC, CU, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)CS::bytes(0, SEGC));
     if (e == cudaSuccess && DIM == 4)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 1, SEGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 1, SEGC, CU, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)CS::bytes(1, SEGC));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC>,
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC, LU, MB>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::bytes(2, SEGC));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev].store(true, std::memory_order_release);
@@ -346,7 +356,7 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   const int X = DIM - 1;
   const long long rows = (long long)G.batch * (G.cells / G.n[X]);
   if (parts & 1) {
-    k_axis_x<SCHEME><<<dim3((unsigned)((rows + AX_THREADS - 1) / AX_THREADS),
+    k_axis_x<SCHEME, XU><<<dim3((unsigned)((rows + AX_THREADS - 1) / AX_THREADS),
                             (unsigned)((G.n[X] + AX_SEG - 1) / AX_SEG)),
                        AX_THREADS, xsmem, s>>>(Q, S);
     e = cudaGetLastError();
@@ -357,9 +367,9 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
     const long long ncol = (long long)G.batch * G.cells / G.n[a];
     return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + SEGC - 1) / SEGC));
   };
-  k_axis_col<SCHEME, HAM, DIM, 0, SEGC><<<grid_of(0), AX_THREADS, CS::bytes(0, SEGC), s>>>(Q, S);
-  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1, SEGC><<<grid_of(1), AX_THREADS, CS::bytes(1, SEGC), s>>>(Q, S);
-  k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC><<<grid_of(DIM - 2), AX_THREADS, CS::bytes(2, SEGC), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, 0, SEGC, CU, MB><<<grid_of(0), AX_THREADS, CS::bytes(0, SEGC), s>>>(Q, S);
+  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1, SEGC, CU, MB><<<grid_of(1), AX_THREADS, CS::bytes(1, SEGC), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC, LU, MB><<<grid_of(DIM - 2), AX_THREADS, CS::bytes(2, SEGC), s>>>(Q, S);
   return cudaGetLastError();
 }
 

@@ -2,9 +2,22 @@
 #include "hj_axes.cuh"
 
 namespace hj {
+int axes_unroll();   // hj_fast.cu
+
 template <int SEGC>
 static cudaError_t axes_weno5(const StageArgs& P, cudaStream_t s, int parts) {
   double* scratch = P.aux0;
+  // A/B variants (the C2 / C4 / C5 Hamiltonians only): every walk rolled (the
+  // round-2 r02g pipeline), or the contiguous-axis walk unrolled as well
+  switch (P.ham.kind == HJ_HAM_DI4 || P.ham.kind == HJ_HAM_AIR3D ? axes_unroll() : -1) {
+    case 0:
+      if (P.g.dim == 4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC, 0>(P, s, scratch, parts);
+      return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC, 0>(P, s, scratch, parts);
+    case 5:
+      if (P.g.dim == 4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC, 5>(P, s, scratch, parts);
+      return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC, 5>(P, s, scratch, parts);
+    default: break;
+  }
   if (P.g.dim == 4) {
     if (P.ham.kind == HJ_HAM_DI4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC>(P, s, scratch, parts);
     return launch_axes_t<HJ_WENO5, HJ_HAM_ADVECTION, 4, SEGC>(P, s, scratch, parts);

@@ -31,10 +31,21 @@ static int stage_variant() {
     if (e && std::string(e) == "brick_x") v = 7;        // A/B slot (hj_brick_weno.cu: the variant under test)
     if (e && std::string(e) == "tile_stages") v = 8;    // small 3-D grids: tile kernel per stage, no persistent launch
     if (e && std::string(e) == "axes") v = 9;           // brick-sized WENO5 grids: the per-axis walk pipeline
+    if (e && std::string(e) == "axes_r1") v = 10;       // per-axis A/B: every walk rolled (the r02g pipeline)
+    if (e && std::string(e) == "axes_u2x") v = 11;      //  ... the contiguous-axis walk unrolled as well
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
   return g_variant.load(std::memory_order_relaxed);
+}
+
+// walk unroll of the per-axis pipeline (launch_axes_t's WU bits)
+int axes_unroll() {
+  switch (stage_variant()) {
+    case 10: return 0;
+    case 11: return 5;
+    default: return -1;
+  }
 }
 
 int set_stage_variant(int v) {
@@ -55,7 +66,7 @@ int set_stage_variant(int v) {
 // axis-0 walk reads exchanged planes).
 bool axes_applies(int scheme, const StageArgs& P, bool allow_halo) {
   const int v = stage_variant();
-  if ((v != 1 && v != 9) || scheme != HJ_WENO5) return false;
+  if ((v != 1 && v != 9 && v < 10) || scheme != HJ_WENO5) return false;
   if ((P.g.dim != 3 && P.g.dim != 4) || P.want_ranges) return false;
   if (!allow_halo && (P.g.ax[0].halo_lo || P.g.ax[0].halo_hi)) return false;
   if (P.zp.lo != 0 || P.zp.cnt != P.g.n[0]) return false;
@@ -140,6 +151,6 @@ bool persist_applies(const StageArgs& P) {
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 9) return -1;
+  if (variant < -1 || variant > 11) return -1;
   return hj::set_stage_variant(variant);
 }

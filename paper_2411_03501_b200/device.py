@@ -28,7 +28,10 @@ STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always"
                  "brick_nopf": 6,     # no L2 prefetch of the next brick (A/B)
                  "brick_x": 7,        # A/B slot: the variant under test (hj_brick_weno.cu)
                  "tile_stages": 8,    # small 3-D grids: the tile kernel launched per stage (no persistent launch)
-                 "axes": 9}           # the per-axis walk pipeline (hj_axes.cuh) forced on every WENO5 grid size
+                 "axes": 9,           # the per-axis walk pipeline (hj_axes.cuh) forced on every WENO5 grid size
+                 # per-axis pipeline A/B: every walk rolled (the r02g default), the
+                 # contiguous-axis walk unrolled too (hj_axes.cuh launch_axes_t)
+                 "axes_r1": 10, "axes_u2x": 11}
 
 
 def set_stage_kernel(name: str) -> str:
