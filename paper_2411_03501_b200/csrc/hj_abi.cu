@@ -404,7 +404,7 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
     // one half of a slab stage on the per-axis walk pipeline (same stream, so
     // the same scratch for both halves)
     if (!axes_applies(scheme, P, true)) return fail(HJ_EINVAL, "stage does not run the per-axis walk pipeline");
-    P.aux0 = scratch_for(s, (size_t)(P.g.dim + 1) * span);
+    P.aux0 = scratch_for(s, axes_scratch_doubles(P.g.dim, span));
     if (!P.aux0) return fail(HJ_ECUDA, "no scratch for the per-axis walk pipeline");
     set_extents(P, g);
     bool handled = false;
@@ -413,8 +413,8 @@ static int stage_impl(const hj_grid* g, int scheme, const hj_ham* ham, const dou
   }
   const bool axes = axes_applies(scheme, P, false);
   if (axes) {
-    // per-axis walk pipeline (hj_axes.cuh): dim + 1 field-sized scratch arrays
-    P.aux0 = scratch_for(s, (size_t)(P.g.dim + 1) * span);
+    // per-axis walk pipeline (hj_axes.cuh): 2 (dim - 1) field-sized scratch arrays
+    P.aux0 = scratch_for(s, axes_scratch_doubles(P.g.dim, span));
   } else if (P.g.dim == 4) {
     // 4-D brick path: scratch for the axis-0 pre-pass (p_avg0, d0)
     double* scratch = scratch_for(s, 2 * span);

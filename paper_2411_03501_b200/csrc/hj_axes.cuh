@@ -17,10 +17,11 @@
 // the stage update, the mask and the flags -- the brick kernel's arithmetic,
 // bit for bit.
 //
-// Scratch (doubles, one field-sized array each, same offsets as the field):
-//   PX, DX            costate / dissipation term of the contiguous axis
-//   P[0 .. dim-3]     costates of axes 0 .. dim-3
-//   D                 running dissipation sum over axes 0 .. (current)
+// Scratch: field-sized arrays of 16-byte records (same node offsets as the
+// field), so the last kernel's ring takes two streams with one copy each:
+//   XR[n]   = (PX, DX)   costate / dissipation term of the contiguous axis
+//   PD_a[n] = (P_a, D_a) costate of axis a, running dissipation sum over
+//                        axes 0 .. a   (a = 0 .. dim-3)
 #pragma once
 #include "hj_brick.cuh"
 
@@ -32,11 +33,14 @@ constexpr int AX_THREADS = 256;
 constexpr int AX_PITCH = AX_THREADS + 1;   // odd pitch: transposed stores conflict-free
 
 struct AxesScratch {
-  double* px;
-  double* dx;
-  double* p[HJ_MAX_DIM];
-  double* d;
+  double2* xr;
+  double2* pd[HJ_MAX_DIM - 2];
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
 
 // ---------------------------------------------------------------- contiguous axis (walked first)
 // CTA = 256 rows x one 16-node segment along the row.  Rows are staged
@@ -103,10 +107,8 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, con
     const long long rr = r0 + tr;
     if (rr >= rows || xl >= zmax) continue;
     const long long o = rr * nx + x0 + xl;
-    HJ_CHK(P, aux, S.px + o, 8);
-    HJ_CHK(P, aux, S.dx + o, 8);
-    S.px[o] = sp[xl * AX_PITCH + tr];
-    S.dx[o] = sd[xl * AX_PITCH + tr];
+    HJ_CHK(P, aux, S.xr + o, 16);
+    S.xr[o] = make_double2(sp[xl * AX_PITCH + tr], sd[xl * AX_PITCH + tr]);
   }
 }
 
@@ -120,7 +122,8 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, con
 // y0 / mask values through a two-node cp.async ring filled two nodes ahead.
 template <int DIM>
 struct AxisColSmem {
-  static constexpr int NS = DIM + 3;   // ring streams: P[0..DIM-3], PX, D, DX, y0, mask
+  // ring doubles per node: XR and PD_{dim-3} records, P_0 (4-D), y0, mask
+  static constexpr int NS = DIM + 3;
   // shared memory of a column kernel with SEGC-node segments: the staged
   // column rows, then the two-node ring (mode 1: D; mode 2: NS streams)
   static constexpr size_t bytes(int mode, int segc) {
@@ -171,10 +174,9 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
     auto emit = [&](int j, double L, double R) {
       if (j < zmax) {
         const long long off = colbase + (long long)(z0 + j) * inner;
-        HJ_CHK(P, aux, S.d + off, 8);
-        HJ_CHK(P, aux, S.p[axis] + off, 8);
-        S.p[axis][off] = 0.5 * (L + R);                                               // term.py:101
-        S.d[off] = 0.0 + ah * (R - L);                                                // term.py:84-86
+        HJ_CHK(P, aux, S.pd[0] + off, 16);
+        S.pd[0][off] = make_double2(0.5 * (L + R),         // term.py:101
+                                    0.0 + ah * (R - L));   // term.py:84-86
       }
     };
     if (on) line_walk<SCHEME, WU, SEGC>(ld, G.sp[axis], emit, zmax);
@@ -183,8 +185,8 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
     auto issue = [&](int j) {
       if (on && j < zmax) {
         const long long off = colbase + (long long)(z0 + j) * inner;
-        HJ_CHK(P, aux, S.d + off, 8);
-        cp_async8(extra + (j & 1) * AX_THREADS + t, S.d + off);
+        HJ_CHK(P, aux, &S.pd[axis - 1][off].y, 8);
+        cp_async8(extra + (j & 1) * AX_THREADS + t, &S.pd[axis - 1][off].y);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -194,9 +196,9 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
       if (j >= zmax) return;
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       const long long off = colbase + (long long)(z0 + j) * inner;
-      HJ_CHK(P, aux, S.p[axis] + off, 8);
-      S.p[axis][off] = 0.5 * (L + R);                                                 // term.py:101
-      S.d[off] = extra[(j & 1) * AX_THREADS + t] + ah * (R - L);                      // term.py:84-86
+      HJ_CHK(P, aux, S.pd[axis] + off, 16);
+      S.pd[axis][off] = make_double2(0.5 * (L + R),                                    // term.py:101
+                                     extra[(j & 1) * AX_THREADS + t] + ah * (R - L));  // term.py:84-86
       issue(j + 2);   // (the slot's value is consumed by the store above)
     };
     if (on) line_walk<SCHEME, WU, SEGC>(ld, G.sp[axis], emit, zmax);
@@ -221,29 +223,28 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
     const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
     const bool need_m = P.mask != HJ_MASK_NONE;
     unsigned flags = 0u;
-    // ring slot (j & 1), stream k: extra[((j & 1) * NS + k) * 256 + t]
+    // ring slot (j & 1) at extra + (j & 1) * NS * 256 doubles: thread t's XR
+    // record at [2t], its PD_{dim-3} record at [512 + 2t], then 8-byte streams
+    // P_0 (4-D) at [1024 + t], y0 at [(DIM + 1) * 256 + t], mask at [(DIM + 2) * 256 + t]
     auto issue = [&](int j) {
       if (on && j < zmax) {
         const long long off = colbase + (long long)(z0 + j) * inner;
-        double* slot = extra + (j & 1) * NS * AX_THREADS + t;
-#pragma unroll
-        for (int a = 0; a < DIM - 2; ++a) {
-          HJ_CHK(P, aux, S.p[a] + off, 8);
-          cp_async8(slot + a * AX_THREADS, S.p[a] + off);
+        double* slot = extra + (j & 1) * NS * AX_THREADS;
+        HJ_CHK(P, aux, S.xr + off, 16);
+        HJ_CHK(P, aux, S.pd[DIM - 3] + off, 16);
+        cp_async16(slot + 2 * t, S.xr + off);                          // (PX, DX)
+        cp_async16(slot + 2 * AX_THREADS + 2 * t, S.pd[DIM - 3] + off);  // (P_{dim-3}, D)
+        if constexpr (DIM == 4) {
+          HJ_CHK(P, aux, &S.pd[0][off].x, 8);
+          cp_async8(slot + 4 * AX_THREADS + t, &S.pd[0][off].x);       // P_0
         }
-        HJ_CHK(P, aux, S.px + off, 8);
-        HJ_CHK(P, aux, S.d + off, 8);
-        HJ_CHK(P, aux, S.dx + off, 8);
-        cp_async8(slot + (DIM - 2) * AX_THREADS, S.px + off);
-        cp_async8(slot + (DIM - 1) * AX_THREADS, S.d + off);
-        cp_async8(slot + DIM * AX_THREADS, S.dx + off);
         if (need_y0) {
           HJ_CHK(P, y0, P.y0 + off, 8);
-          cp_async8(slot + (DIM + 1) * AX_THREADS, P.y0 + off);
+          cp_async8(slot + (DIM + 1) * AX_THREADS + t, P.y0 + off);
         }
         if (need_m) {
           HJ_CHK(P, mask, mp + off, 8);
-          cp_async8(slot + (DIM + 2) * AX_THREADS, mp + off);
+          cp_async8(slot + (DIM + 2) * AX_THREADS + t, mp + off);
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -254,6 +255,8 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
       if (j >= zmax) return;
       asm volatile("cp.async.wait_group 1;" ::: "memory");   // node j's copies have landed
       const double* slot = extra + (j & 1) * NS * AX_THREADS + t;
+      const double2 xr = reinterpret_cast<const double2*>(extra + (j & 1) * NS * AX_THREADS)[t];
+      const double2 pd = reinterpret_cast<const double2*>(extra + (j & 1) * NS * AX_THREADS + 2 * AX_THREADS)[t];
       const long long off = colbase + (long long)(z0 + j) * inner;
       // H's node-table inputs: the column's constant ones were read once
       // (cin below); only the walk axis' coordinate changes per node
@@ -261,12 +264,12 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
       if constexpr ((HAM == HJ_HAM_ROCKETS || HAM == HJ_HAM_ROCKETS_EXTREMAL) && axis == 0) cin[0] = G.nodes[0][z0 + j];
       if constexpr (HAM == HJ_HAM_DI4 && axis == 2) cin[0] = G.nodes[2][z0 + j];
       double pv[DIM];
-#pragma unroll
-      for (int a = 0; a < DIM - 2; ++a) pv[a] = slot[a * AX_THREADS];
+      if constexpr (DIM == 4) pv[0] = slot[4 * AX_THREADS];
+      pv[DIM - 3] = pd.x;
       pv[DIM - 2] = 0.5 * (L + R);                                           // term.py:101
-      pv[DIM - 1] = slot[(DIM - 2) * AX_THREADS];
+      pv[DIM - 1] = xr.x;
       // term.py:84-86 order: (((0 + d0) + ...) + d_{dim-2}) + d_{dim-1}
-      const double dsum = (slot[(DIM - 1) * AX_THREADS] + ah * (R - L)) + slot[DIM * AX_THREADS];
+      const double dsum = (pd.y + ah * (R - L)) + xr.y;
       const double H = ham_eval<HAM, DIM>(P.ham, cin, pv);
       if (P.want_hnz && H != 0.0) flags |= HJ_FLAG_HAM_NONZERO;
       const double delta = dsum - H;                                         // term.py:113
@@ -326,10 +329,8 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
   AxesScratch S{};
-  S.px = scratch;
-  S.dx = scratch + span;
-  S.d = scratch + 2 * span;
-  for (int a = 0; a < DIM - 2; ++a) S.p[a] = scratch + (3 + a) * span;
+  S.xr = reinterpret_cast<double2*>(scratch);
+  for (int a = 0; a < DIM - 2; ++a) S.pd[a] = reinterpret_cast<double2*>(scratch + 2 * (1 + a) * span);
   const size_t xsmem = (size_t)(AX_ROWS + 2 * AX_SEG) * AX_PITCH * sizeof(double);
   using CS = AxisColSmem<DIM>;
   static std::atomic<bool> configured[64];
@@ -352,7 +353,7 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
   }
   // the scratch is this path's "aux" extent (bounds-checking build)
   StageArgs Q = P;
-  Q.bc.aux = Extent{scratch, scratch + (DIM + 1) * span};
+  Q.bc.aux = Extent{scratch, scratch + axes_scratch_doubles(DIM, (size_t)span)};
   const int X = DIM - 1;
   const long long rows = (long long)G.batch * (G.cells / G.n[X]);
   if (parts & 1) {

@@ -60,7 +60,7 @@ int set_stage_variant(int v) {
 // of 3-D / 4-D grids (no exchanged halos, contiguous batches, no range
 // statistics) -- by default those of brick size (measured faster than the
 // brick kernels at 301^3, 121^4 and 8 x 101^3: DESIGN.md); "axes" forces it
-// on every size (tests).  It needs (dim + 1) field-sized scratch arrays.
+// on every size (tests).  It needs 2 (dim - 1) field-sized scratch arrays.
 // allow_halo: a multi-GPU slab stage split around its halo exchange
 // (hj_dd_stage: the contiguous-axis kernel overlaps the exchange; only the
 // axis-0 walk reads exchanged planes).

@@ -87,6 +87,13 @@ struct PersistArgs {
   PersistStage st[PERSIST_MAX_STAGES];
 };
 
+// doubles of device scratch the per-axis walk pipeline (hj_axes.cuh) needs
+// for a field of `span` nodes: 16-byte records (PX, DX) and (P_a, D_a),
+// a = 0 .. dim-3
+__host__ __device__ constexpr size_t axes_scratch_doubles(int dim, size_t span) {
+  return (size_t)2 * (size_t)(dim - 1) * span;
+}
+
 #ifdef HJ_CHECK_BOUNDS
 __device__ __forceinline__ void chk_extent(const BoundsCheck& b, const Extent& e, const void* p, int bytes,
                                            const char* what, const char* file, int line) {
