@@ -77,6 +77,9 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhjb200.
 # HJ_LIB=check selects the bounds-checking build (libhjb200_check.so, build.py --check)
 if os.environ.get("HJ_LIB") == "check":
     _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhjb200_check.so")
+# HJ_LIB_PATH: an explicit build of the library (A/B of two builds in one process tree, scripts/)
+if os.environ.get("HJ_LIB_PATH"):
+    _LIB_PATH = os.environ["HJ_LIB_PATH"]
 
 # (name, restype, argtypes) -- must match include/hjb200.h
 _SIGNATURES = [
