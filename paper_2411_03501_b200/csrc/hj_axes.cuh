@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
 template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG, int WU = 4>
 static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch, int parts = 3) {
   constexpr int XU = (WU & 1) ? 2 : 1, LU = (WU & 2) ? 2 : 1, CU = (WU & 4) ? 2 : 1, MB = (WU & 8) ? 3 : 2;
+  constexpr int LSEG = (WU & 16) ? 2 * SEGC : SEGC;   // bit 4: the last-axis kernel walks 2 SEGC-node segments
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
   AxesScratch S{};
@@ -346,8 +347,8 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
       e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, 1, SEGC, CU, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)CS::bytes(1, SEGC));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC, LU, MB>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::bytes(2, SEGC));
+      e = cudaFuncSetAttribute(k_axis_col<SCHEME, HAM, DIM, DIM - 2, LSEG, LU, MB>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::bytes(2, LSEG));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev].store(true, std::memory_order_release);
   }
@@ -364,13 +365,13 @@ static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scr
     if (e != cudaSuccess) return e;
   }
   if (!(parts & 2)) return cudaSuccess;
-  auto grid_of = [&](int a) {
+  auto grid_of = [&](int a, int seg) {
     const long long ncol = (long long)G.batch * G.cells / G.n[a];
-    return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + SEGC - 1) / SEGC));
+    return dim3((unsigned)((ncol + AX_THREADS - 1) / AX_THREADS), (unsigned)((G.n[a] + seg - 1) / seg));
   };
-  k_axis_col<SCHEME, HAM, DIM, 0, SEGC, CU, MB><<<grid_of(0), AX_THREADS, CS::bytes(0, SEGC), s>>>(Q, S);
-  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1, SEGC, CU, MB><<<grid_of(1), AX_THREADS, CS::bytes(1, SEGC), s>>>(Q, S);
-  k_axis_col<SCHEME, HAM, DIM, DIM - 2, SEGC, LU, MB><<<grid_of(DIM - 2), AX_THREADS, CS::bytes(2, SEGC), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, 0, SEGC, CU, MB><<<grid_of(0, SEGC), AX_THREADS, CS::bytes(0, SEGC), s>>>(Q, S);
+  if constexpr (DIM == 4) k_axis_col<SCHEME, HAM, DIM, 1, SEGC, CU, MB><<<grid_of(1, SEGC), AX_THREADS, CS::bytes(1, SEGC), s>>>(Q, S);
+  k_axis_col<SCHEME, HAM, DIM, DIM - 2, LSEG, LU, MB><<<grid_of(DIM - 2, LSEG), AX_THREADS, CS::bytes(2, LSEG), s>>>(Q, S);
   return cudaGetLastError();
 }
 

@@ -16,6 +16,9 @@ static cudaError_t axes_weno5(const StageArgs& P, cudaStream_t s, int parts) {
     case 5:
       if (P.g.dim == 4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC, 5>(P, s, scratch, parts);
       return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC, 5>(P, s, scratch, parts);
+    case 20:
+      if (P.g.dim == 4) return launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, SEGC, 20>(P, s, scratch, parts);
+      return launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, SEGC, 20>(P, s, scratch, parts);
     default: break;
   }
   if (P.g.dim == 4) {

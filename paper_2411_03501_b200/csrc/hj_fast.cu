@@ -33,6 +33,7 @@ static int stage_variant() {
     if (e && std::string(e) == "axes") v = 9;           // brick-sized WENO5 grids: the per-axis walk pipeline
     if (e && std::string(e) == "axes_r1") v = 10;       // per-axis A/B: every walk rolled (the r02g pipeline)
     if (e && std::string(e) == "axes_u2x") v = 11;      //  ... the contiguous-axis walk unrolled as well
+    if (e && std::string(e) == "axes_l32") v = 12;      //  ... the last-axis kernel on 32-node segments
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
@@ -44,6 +45,7 @@ int axes_unroll() {
   switch (stage_variant()) {
     case 10: return 0;
     case 11: return 5;
+    case 12: return 20;
     default: return -1;
   }
 }
@@ -151,6 +153,6 @@ bool persist_applies(const StageArgs& P) {
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 11) return -1;
+  if (variant < -1 || variant > 12) return -1;
   return hj::set_stage_variant(variant);
 }

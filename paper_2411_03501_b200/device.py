@@ -31,7 +31,8 @@ STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always"
                  "axes": 9,           # the per-axis walk pipeline (hj_axes.cuh) forced on every WENO5 grid size
                  # per-axis pipeline A/B: every walk rolled (the r02g default), the
                  # contiguous-axis walk unrolled too (hj_axes.cuh launch_axes_t)
-                 "axes_r1": 10, "axes_u2x": 11}
+                 "axes_r1": 10, "axes_u2x": 11,
+                 "axes_l32": 12}      # ... the last-axis kernel on 32-node segments
 
 
 def set_stage_kernel(name: str) -> str:
