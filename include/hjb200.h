@@ -285,7 +285,9 @@ int hj_check_division(int64_t n, uint64_t seed, unsigned long long* d_mismatch, 
  * global->shared loads: WRONG results), 6 brick kernels without the L2
  * prefetch of the next brick, 7 the brick A/B slot, 8 small 3-D grids: tile
  * kernel per stage (no persistent launch), 9 the per-axis walk pipeline for
- * every WENO5 grid size; -1 reads HJ_STAGE_KERNEL from the environment.
+ * every WENO5 grid size, 10-12 per-axis pipeline A/B variants (10 every walk
+ * rolled, 11 the contiguous-axis walk unrolled as well, 12 the last-axis
+ * kernel on 32-node segments); -1 reads HJ_STAGE_KERNEL from the environment.
  * Returns the previous setting. */
 int hj_set_stage_kernel(int variant);
 /* FP64-pipe probe for the roofline denominator: blocks x 256 threads each run
