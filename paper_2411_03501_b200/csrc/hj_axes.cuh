@@ -29,7 +29,12 @@ namespace hj {
 
 constexpr int AX_SEG = 16;                 // nodes per walk segment
 constexpr int AX_ROWS = AX_SEG + 6;        // staged rows per segment (halo 3 + 3)
-constexpr int AX_THREADS = 256;
+// 128-thread CTAs, 4 per SM (128 registers, 16 warps per SM as before): the
+// CTAs' staging / walk / write-back phases desynchronise over twice as many
+// CTAs (A/B against 256 x 2 on one B200: C2 +3.4 %, C4 +3.4 %, C5 +4.1 %,
+// profiles/r02_raw/kernel_variant_ab.txt abb3)
+constexpr int AX_THREADS = 128;
+constexpr int AX_CTAS = 4;   // resident CTAs per SM the kernels are compiled for
 constexpr int AX_PITCH = AX_THREADS + 1;   // odd pitch: transposed stores conflict-free
 
 struct AxesScratch {
@@ -43,14 +48,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 // ---------------------------------------------------------------- contiguous axis (walked first)
-// CTA = 256 rows x one 16-node segment along the row.  Rows are staged
+// CTA = AX_THREADS rows x one 16-node segment along the row.  Rows are staged
 // transposed (warp w loads rows 32w .. 32w+31, lanes along the row: 22
 // consecutive doubles per load), thread t walks row t from shared memory, the
 // (p, d) results are staged and written back row-wise (coalesced).
 // WU: walk steps per loop iteration (2: the window state rolls through
 // renamed registers instead of moves; hj_weno_line.cuh)
 template <int SCHEME, int WU = 1>
-__global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, const AxesScratch S) {
+__global__ void __launch_bounds__(AX_THREADS, AX_CTAS) k_axis_x(const StageArgs P, const AxesScratch S) {
   extern __shared__ __align__(16) double axs[];
   double* stg = axs;                                  // [AX_ROWS][AX_PITCH]
   double* sp = axs + AX_ROWS * AX_PITCH;              // [AX_SEG][AX_PITCH]
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(AX_THREADS, 2) k_axis_x(const StageArgs P, con
 // MODE 0: first (D = 0 + d_a), 1: accumulate (D = D + d_a), 2: last, fused
 // with the node update.  Columns: position p = o * inner + i (inner = the
 // axis' stride, o = everything before the axis, batch included); a CTA takes
-// 256 consecutive positions (coalesced) and one 16-node segment.  Per-node
+// AX_THREADS consecutive positions (coalesced) and one 16-node segment.  Per-node
 // global inputs never sit on the walk's critical path: mode 1 stages the
 // segment's D with the column (cp.async), mode 2 streams the node's scratch /
 // y0 / mask values through a two-node cp.async ring filled two nodes ahead.
@@ -132,13 +137,13 @@ struct AxisColSmem {
   }
 };
 
-template <int SCHEME, int HAM, int DIM, int AXIS, int SEGC, int WU = 1, int MINB = 2>
+template <int SCHEME, int HAM, int DIM, int AXIS, int SEGC, int WU = 1, int MINB = AX_CTAS>
 __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P, const AxesScratch S) {
   constexpr int axis = AXIS;
   constexpr int MODE = (AXIS == DIM - 2) ? 2 : (AXIS == 0 ? 0 : 1);
   constexpr int NS = AxisColSmem<DIM>::NS;
   constexpr int ROWS = SEGC + 6;
-  extern __shared__ __align__(16) double cs[];   // [ROWS][256] column, then the ring (modes 1, 2)
+  extern __shared__ __align__(16) double cs[];   // [ROWS][AX_THREADS] column, then the ring (modes 1, 2)
   double* const extra = cs + ROWS * AX_THREADS;
   const GridArgs& G = P.g;
   const long long inner = G.stride[axis];
@@ -223,9 +228,9 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
     const bool need_y0 = P.stage >= HJ_STAGE_RK2_AVG;
     const bool need_m = P.mask != HJ_MASK_NONE;
     unsigned flags = 0u;
-    // ring slot (j & 1) at extra + (j & 1) * NS * 256 doubles: thread t's XR
-    // record at [2t], its PD_{dim-3} record at [512 + 2t], then 8-byte streams
-    // P_0 (4-D) at [1024 + t], y0 at [(DIM + 1) * 256 + t], mask at [(DIM + 2) * 256 + t]
+    // ring slot (j & 1) at extra + (j & 1) * NS * T doubles (T = AX_THREADS):
+    // thread t's XR record at [2t], its PD_{dim-3} record at [2T + 2t], then
+    // 8-byte streams P_0 (4-D) at [4T + t], y0 at [(DIM + 1) T + t], mask at [(DIM + 2) T + t]
     auto issue = [&](int j) {
       if (on && j < zmax) {
         const long long off = colbase + (long long)(z0 + j) * inner;
@@ -318,14 +323,15 @@ __global__ void __launch_bounds__(AX_THREADS, MINB) k_axis_col(const StageArgs P
 // stage launches them on either side of its halo exchange, hj_dd_stage)
 // WU: walk two steps per loop iteration in the contiguous-axis kernel (bit 0),
 // the last-axis kernel (bit 1), the axis-0 / middle-axis column kernels (bit
-// 2); bit 3: column kernels compiled for 3 CTAs per SM.  Default: bit 2 only
+// 2); bit 3: column kernels compiled for 3 CTAs per SM (measured with
+// 256-thread CTAs: 80 registers, spills, -32 .. -40 %; not instantiated);
+// bit 4: the last-axis kernel on 2 SEGC-node segments.  Default: bit 2 only
 // (A/B on one B200, profiles/r02_raw/kernel_variant_ab.txt: C2 +1.9 %, C4
 // +1.9 %, C5 +-0; the unrolled contiguous-axis walk: C2 +2.0 %, C4 -4.7 %,
-// C5 -0.6 %; the unrolled last-axis walk -0.4 .. -1.2 %; 3 CTAs per SM spill
-// at 80 registers: -32 .. -40 %)
+// C5 -0.6 %; the unrolled last-axis walk -0.4 .. -1.2 %)
 template <int SCHEME, int HAM, int DIM, int SEGC = AX_SEG, int WU = 4>
 static cudaError_t launch_axes_t(const StageArgs& P, cudaStream_t s, double* scratch, int parts = 3) {
-  constexpr int XU = (WU & 1) ? 2 : 1, LU = (WU & 2) ? 2 : 1, CU = (WU & 4) ? 2 : 1, MB = (WU & 8) ? 3 : 2;
+  constexpr int XU = (WU & 1) ? 2 : 1, LU = (WU & 2) ? 2 : 1, CU = (WU & 4) ? 2 : 1, MB = (WU & 8) ? 3 : AX_CTAS;
   constexpr int LSEG = (WU & 16) ? 2 * SEGC : SEGC;   // bit 4: the last-axis kernel walks 2 SEGC-node segments
   const GridArgs& G = P.g;
   const long long span = (long long)G.batch_stride * (G.batch - 1) + G.cells;
