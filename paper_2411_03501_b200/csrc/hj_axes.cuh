@@ -1,5 +1,6 @@
 // hj_axes.cuh -- the fused LF + TVD-RK stage as a pipeline of single-axis
-// walks ("axes" path): one kernel per grid axis, each walking 16-node column
+// walks ("axes" path): one kernel per grid axis, each walking 16-node (the
+// contiguous axis) or 32-node (the column axes, hj_axes_weno.cu) column
 // segments of its axis from a shared-memory stage (all loads in flight at
 // once), the last one fused with the node update.
 //

@@ -34,9 +34,17 @@ static cudaError_t axes_weno5(const StageArgs& P, cudaStream_t s, int parts) {
   }
 }
 
-// (32-node column segments measured +1.5 % C4, -1.8 % C5, -0.2 % C2: 16 kept)
+// Column kernels walk 32-node segments (AX_SEGC), the contiguous-axis kernel
+// 16-node ones (AX_SEG): with 128-thread CTAs the halved window-fill work
+// pays (A/B on one B200: C2 +1.2 %, C4 +2.8 %, C5 +0.9 %; with 256-thread
+// CTAs it had measured +1.5 % C4, -1.8 % C5, -0.2 % C2)
+constexpr int AX_SEGC = 2 * AX_SEG;
+
 cudaError_t launch_axes_weno5(const StageArgs& P, cudaStream_t s, bool* handled, int parts) {
   *handled = true;
-  return axes_weno5<AX_SEG>(P, s, parts);
+  if (axes_unroll() == 64 && (P.ham.kind == HJ_HAM_DI4 || P.ham.kind == HJ_HAM_AIR3D))   // A/B "axes_s16"
+    return P.g.dim == 4 ? launch_axes_t<HJ_WENO5, HJ_HAM_DI4, 4, AX_SEG>(P, s, P.aux0, parts)
+                        : launch_axes_t<HJ_WENO5, HJ_HAM_AIR3D, 3, AX_SEG>(P, s, P.aux0, parts);
+  return axes_weno5<AX_SEGC>(P, s, parts);
 }
 }  // namespace hj

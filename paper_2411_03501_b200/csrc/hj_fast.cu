@@ -34,6 +34,7 @@ static int stage_variant() {
     if (e && std::string(e) == "axes_r1") v = 10;       // per-axis A/B: every walk rolled (the r02g pipeline)
     if (e && std::string(e) == "axes_u2x") v = 11;      //  ... the contiguous-axis walk unrolled as well
     if (e && std::string(e) == "axes_l32") v = 12;      //  ... the last-axis kernel on 32-node segments
+    if (e && std::string(e) == "axes_s16") v = 13;      //  ... column kernels on 16-node segments
     int expect = -1;
     g_variant.compare_exchange_strong(expect, v);
   }
@@ -46,6 +47,7 @@ int axes_unroll() {
     case 10: return 0;
     case 11: return 5;
     case 12: return 20;
+    case 13: return 64;
     default: return -1;
   }
 }
@@ -153,6 +155,6 @@ bool persist_applies(const StageArgs& P) {
 }  // namespace hj
 
 extern "C" int hj_set_stage_kernel(int variant) {
-  if (variant < -1 || variant > 12) return -1;
+  if (variant < -1 || variant > 13) return -1;
   return hj::set_stage_variant(variant);
 }

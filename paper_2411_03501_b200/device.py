@@ -32,7 +32,8 @@ STAGE_KERNELS = {"env": -1, "generic": 0, "auto": 1, "brick1": 2, "brick_always"
                  # per-axis pipeline A/B: every walk rolled (the r02g default), the
                  # contiguous-axis walk unrolled too (hj_axes.cuh launch_axes_t)
                  "axes_r1": 10, "axes_u2x": 11,
-                 "axes_l32": 12}      # ... the last-axis kernel on 32-node segments
+                 "axes_l32": 12,      # ... the last-axis kernel on 32-node segments
+                 "axes_s16": 13}      # ... column kernels on 16-node segments (the default is 32)
 
 
 def set_stage_kernel(name: str) -> str:

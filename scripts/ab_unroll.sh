@@ -4,7 +4,7 @@
 # GPU parity tests of the per-axis kernel family.
 TAG=${1:-abu}
 for cfg in c2 c5 c4; do
-  timeout 900 python scripts/variant_probe.py $cfg auto axes_u2x auto > gpurun_out/${TAG}_ab_$cfg.log 2>&1
+  timeout 900 python scripts/variant_probe.py $cfg auto axes_s32 auto > gpurun_out/${TAG}_ab_$cfg.log 2>&1
 done
 [ -n "$SKIP_TESTS" ] || { timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_tests.log 2>&1; echo "rc $?" >> gpurun_out/${TAG}_tests.log; }
 echo done
