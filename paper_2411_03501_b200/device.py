@@ -59,12 +59,22 @@ def to_dev(a) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device())
 
 
+def host_empty(shape, dtype=torch.float64) -> torch.Tensor:
+    """Host buffer for device copies: pinned (direct DMA) when the OS lets the
+    process lock that much memory, else pageable (the copy is then staged by
+    the driver -- slower, same bytes)."""
+    try:
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+    except RuntimeError:   # cudaHostAlloc refused (locked-memory limit / host RAM)
+        return torch.empty(shape, dtype=dtype)
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     """Device tensor -> numpy.  Large fields land in pinned host memory (torch's
     caching host allocator) so the copy is a direct DMA, not a staged one."""
     t = t.detach()
     if t.is_cuda and t.numel() * t.element_size() >= (1 << 20):
-        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out = host_empty(t.shape, t.dtype)
         out.copy_(t)
         return out.numpy()
     return t.cpu().numpy()

@@ -235,7 +235,7 @@ class FusedIntegrator:
                                                 for k in range(len(kinds))])
         _, bufs, s_in, s_out, s_st = self._pipe
         y_dev = bufs[0]
-        out_host = torch.empty(shape, dtype=dev.F64, pin_memory=True)
+        out_host = dev.host_empty(shape, dev.F64)
         src_host = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
         staged = None
         if not src_host.is_pinned():
@@ -290,7 +290,7 @@ class FusedIntegrator:
         from concurrent.futures import ThreadPoolExecutor
 
         if getattr(self, "_staging", None) is None or self._staging.shape != src.shape:
-            self._staging = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            self._staging = dev.host_empty(src.shape, src.dtype)
         if getattr(self, "_stage_pool", None) is None:
             self._stage_pool = ThreadPoolExecutor(max_workers=int(self.staging_threads),
                                                   thread_name_prefix="hj-stage")

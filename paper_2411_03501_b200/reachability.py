@@ -204,7 +204,7 @@ class SnapshotPipe:
 
     def push(self, k, t, state: torch.Tensor) -> None:
         if state.numel() * state.element_size() < self.SMALL:
-            host = torch.empty(state.shape, dtype=state.dtype, pin_memory=True)
+            host = dev.host_empty(state.shape, state.dtype)
             self.copy.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(self.copy):
                 host.copy_(state, non_blocking=True)
@@ -348,7 +348,7 @@ def _batch_runner(g: Grid, cfg: TermConfig, batch: int):
     hit = per.get(key)
     if hit is None or hit[0] is not cfg:
         fi = FusedIntegrator(g, cfg, dg=dev.DeviceGrid(g, batch=batch))
-        staging = torch.empty((batch,) + tuple(g.counts), dtype=dev.F64, pin_memory=True)
+        staging = dev.host_empty((batch,) + tuple(g.counts), dev.F64)
         hit = (cfg, fi, staging, ThreadPoolExecutor(max_workers=8, thread_name_prefix="hj-batch"))
         per.clear()   # one batch shape per grid is kept
         per[key] = hit
@@ -392,7 +392,7 @@ def _solve_batch_streamed(g: Grid, arrs, cfg: TermConfig, horizon: float, order:
     bounds = [n0 * k // parts for k in range(parts + 1)]
     futs = [[pool.submit(np.copyto, st[b, bounds[k]:bounds[k + 1]], a[bounds[k]:bounds[k + 1]])
              for k in range(parts)] for b, a in enumerate(arrs)]
-    out = torch.empty((B,) + tuple(g.counts), dtype=dev.F64, pin_memory=True)
+    out = dev.host_empty((B,) + tuple(g.counts), dev.F64)
     main = torch.cuda.current_stream()
     for b in range(B):
         s = streams[b]
